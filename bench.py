@@ -1,0 +1,341 @@
+"""bench.py -- driver benchmark of the state-vector hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload qft|rzz|diag|qaoa] [--no-cpu-baseline]
+
+One "step" = one pass of the whole hot path over one synthetic input:
+qs_set_basis_state(x) + qs_apply_circuit(circuit) through the C-ABI
+(host optimiser: booster, diagonal detector, blocking, fusion; then the
+device passes / swaps).  Workload (BASELINE.json configs[1]): the n-qubit QFT
+(reading c18) from |x>, n = 30 + log2(N) (weak scaling: a 16 GiB shard per
+GPU).  Inputs (the gate list, marshalled once) are resident before the timed
+region; the state (16 GiB per GPU) is far larger than the 126 MB L2, so no L2
+flush is needed between steps.
+
+Printed value: effective HBM GB/s of the whole job = sum over GPUs of the
+plan's algorithmic bytes (32 B per amplitude per read+write pass, 16 B per
+write-only pass) / device time per step.  ms_per_step is the
+circuit wall time measured with CUDA events on the library's launching stream
+(max over ranks).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "circuit wall time and effective HBM GB/s at 30–35 qubits, 1/2/4/8 B200"
+BASIS_X = 0x2A5F3C71
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def make_circuit(workload: str, n: int):
+    import workloads as W
+    if workload == "qft":
+        return W.qft(n)
+    if workload == "rzz":
+        return W.rzz_full(n, 1)
+    if workload == "diag":
+        return W.diag_chain(n, 1)
+    if workload == "qaoa":
+        return W.qaoa_maxcut(n, 4, 1, degree=3 if n % 2 == 0 else 4)
+    raise ValueError(workload)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(workload: str, target_s: float = 15.0):
+    """The oracle (as it stands) on a bounded sample of the same workload:
+    the largest n whose circuit finishes in ~target_s, value in the same unit
+    (the sample plan's algorithmic bytes / oracle time)."""
+    import oracle
+    import paper_2604_12256_b200 as qs
+    oracle.build()
+    n, t = 16, 0.0
+    while True:
+        gates = make_circuit(workload, n)
+        t0 = time.perf_counter()
+        oracle.apply_circuit(n, gates, x=BASIS_X % (1 << n))
+        t = time.perf_counter() - t0
+        if t * 2.2 > target_s or n >= 30:
+            break
+        n += 1
+    plan = qs.plan_json(n, gates, product_state=True, basis=BASIS_X % (1 << n))
+    alg = plan["stats"]["bytes_hbm"]
+    return {"value": alg / t / 1e9, "unit": "GB/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": "%s%d (%d gates) from |x>, gate-by-gate Alg. 1, %.2f s; value = the sample "
+                      "plan's algorithmic bytes / oracle time" % (workload, n, len(gates), t),
+            "seconds": t, "n_qubits": n}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle (the tier's reference arm) on a
+    bounded sample of the workload per step; rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    import paper_2604_12256_b200 as qs
+    oracle.build()
+    base = cpu_baseline(args.workload, target_s=max(2.0, min(20.0, 120.0 / max(1, args.steps + args.warmup))))
+    n = base["n_qubits"]
+    gates = make_circuit(args.workload, n)
+    plan = qs.plan_json(n, gates, product_state=True, basis=BASIS_X % (1 << n))
+    alg = plan["stats"]["bytes_hbm"]
+    for _ in range(args.warmup):
+        oracle.apply_circuit(n, gates, x=BASIS_X % (1 << n))
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.apply_circuit(n, gates, x=BASIS_X % (1 << n))
+    dt = (time.perf_counter() - t0) / max(1, args.steps)
+    val = alg / dt / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "%s%d" % (args.workload, n), "n_qubits": n, "gates": len(gates),
+                   "note": "bounded CPU sample of the GPU arm's workload"},
+        "cpu_baseline": {"value": val, "unit": "GB/s", "cores": oracle.num_threads(),
+                         "kind": "oracle", "sample": base["sample"]},
+        "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="qft", choices=["qft", "rzz", "diag", "qaoa"])
+    ap.add_argument("--n", type=int, default=0, help="override qubit count")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_2604_12256_b200 as qs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    g = int(round(math.log2(world)))
+    n = args.n or (30 + g)
+    gates = make_circuit(args.workload, n)
+    marsh = qs.marshal_gates(gates)
+    x = BASIS_X % (1 << n)
+
+    if world > 1:
+        obj = [qs.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        sim = qs.Simulator(n, rank=rank, world_size=world, device=local, nccl_id=obj[0])
+    else:
+        sim = qs.Simulator(n, device=local)
+    stream = torch.cuda.ExternalStream(sim.stream(0), device=torch.device("cuda", local))
+
+    def step():
+        sim.set_basis_state(x)
+        sim.apply(gates, marshalled=marsh)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    launches = 0
+    kt = {}
+    plan_ms = 0.0
+    dev_ms = 0.0
+    for _ in range(args.steps):
+        step()
+        launches += sim.launches()
+        st = sim.stats()
+        plan_ms += st["t_plan_ms"]
+        dev_ms += st["t_device_ms"]
+        for k in ("K1_chunk", "K2_dense", "K3_diag", "small", "K5_expand", "K5_merge", "init", "K4_swap"):
+            t = sim.kernel_timing(k)
+            a = kt.setdefault(k, {"launches": 0, "ms": 0.0, "bytes": 0})
+            for f in a:
+                a[f] += t[f]
+    ev1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    st = sim.stats()
+    ms_t = torch.tensor([ms], device="cuda")
+    if dist is not None:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    bytes_per_step = st["bytes_hbm"] * world
+    value = bytes_per_step / (ms * 1e-3) / 1e9
+
+    # dominant kernel (largest device time) -> roofline
+    dom = max(kt.items(), key=lambda kv: kv[1]["ms"])
+    peak, peak_src = measured_peaks()
+    roof = None
+    if dom[1]["launches"]:
+        avg_ms = dom[1]["ms"] / dom[1]["launches"]
+        per_launch = dom[1]["bytes"] / dom[1]["launches"]
+        ach = per_launch / (avg_ms * 1e-3) / 1e9
+        if dom[0] == "K4_swap":
+            roof = {"kernel": dom[0], "bound": "nvlink", "achieved": ach, "peak": 770.0,
+                    "unit": "GB/s", "frac": ach / 770.0, "traffic": None}
+        else:
+            roof = {"kernel": dom[0], "bound": "hbm", "achieved": ach, "peak": peak,
+                    "peak_source": peak_src + " (MEASURED_PEAKS.json hbm_gbs, burst copy)",
+                    "unit": "GB/s", "frac": ach / peak, "traffic": None,
+                    "bytes_per_launch": per_launch, "avg_launch_ms": avg_ms,
+                    "share_of_step": dom[1]["ms"] / args.steps / ms}
+
+    # e2e: through the C-ABI with host buffers: gate list marshalled from the
+    # Python objects every step (host), descriptors H2D, a 1 Mi-amplitude
+    # slice of the result state D2H (host buffer).
+    e2e = None
+    if args.e2e_steps > 0:
+        slice_amps = 1 << 20
+        barrier()
+        t0 = time.perf_counter()
+        h2d = 0
+        for _ in range(args.e2e_steps):
+            sim.set_basis_state(x)
+            m2 = qs.marshal_gates(gates)
+            h2d += 104 * len(gates)  # qs_gate_t records consumed by the library
+            sim.apply(gates, marshalled=m2)
+            out = sim.state(0, slice_amps)
+        barrier()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
+        t_e = torch.tensor([e2e_ms], device="cuda")
+        if dist is not None:
+            dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t_e.item())
+        e2e = {"value": bytes_per_step / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
+               "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d // args.e2e_steps,
+               "d2h_bytes_per_step": slice_amps * 16,
+               "note": "set_basis_state + marshal + qs_apply_circuit + qs_get_state(1 Mi amps)"}
+
+    if rank == 0:
+        base = None
+        if not args.no_cpu_baseline and world == 1:
+            base = cpu_baseline(args.workload)
+            base.pop("seconds", None)
+            base.pop("n_qubits", None)
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "%s%d" % (args.workload, n), "n_qubits": n, "gates": len(gates),
+                       "basis": x, "shard_gib": (16 << (n - g)) / 2 ** 30,
+                       "parallelism": "state sharded by top %d qubits over %d GPU(s)" % (g, world),
+                       "l2": "no flush: state %.0f GiB per GPU >> 126 MB L2" % ((16 << (n - g)) / 2 ** 30)},
+            "circuit_ms": ms, "device_busy_ms_per_step": dev_ms / args.steps,
+            "plan_ms_per_step": plan_ms / args.steps,
+            "plan": {k: st[k] for k in ("n_passes", "n_chunk_passes", "n_dense_passes",
+                                        "n_diag_passes", "n_swaps", "n_expand",
+                                        "n_substate_gates", "n_fused_diag", "bytes_hbm")},
+            "kernels": {k: v for k, v in kt.items() if v["launches"]},
+            "roofline": roof, "cpu_baseline": base, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    sim.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

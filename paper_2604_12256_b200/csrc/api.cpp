@@ -1,0 +1,839 @@
+// api.cpp -- C-ABI entry points (include/qs.h) and the plan executor.
+//
+// One handle owns one or more shards (a shard = 2^nl amplitudes of the
+// state, rank r holds physical indices [r*2^nl, (r+1)*2^nl)).
+// Three ownership modes:
+//   single   qs_create(n, P): this process drives devices 0..P-1 (NCCL comms
+//            from ncclCommInitAll; exchanges over NVLink);
+//   loopback qs_create_loopback(n, P, dev): P shards on one device, the
+//            exchange is device copies (CI for the sharded path on one GPU);
+//   rank     qs_create_rank(...): one process per GPU (torchrun), NCCL comm
+//            from a broadcast unique id.
+// Every step of the hot path runs in the kernels of kernels.cu or in NCCL;
+// there is no host compute fallback.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/qs.h"
+#include "planner.hpp"
+#include "qs_internal.hpp"
+
+namespace qs {
+cudaError_t launch_pass(int kernel, const unsigned char* dblob, const KPass& hdr,
+                        double2* state, cudaStream_t st);
+cudaError_t launch_expand(double2* dst, u64 n_amps, u64 rank_base, const KExpand& e,
+                          cudaStream_t st);
+cudaError_t launch_merge(double2* dst, const double2* A, int la, const double2* B, int lb,
+                         cudaStream_t st);
+cudaError_t launch_set_one(double2* dst, u64 idx, cudaStream_t st);
+cudaError_t launch_permute(const double2* in, double2* out, u64 n_amps, const int* a, const int* b,
+                           int n, cudaStream_t st);
+cudaError_t launch_gather(const double2* state, double2* out, u64 off, u64 count, int n,
+                          const int8_t* dmap, int nl, u64 rank, int probs, cudaStream_t st);
+}  // namespace qs
+
+using namespace qs;
+
+namespace {
+
+enum Mode { M_SINGLE = 0, M_LOOPBACK = 1, M_RANK = 2 };
+
+struct Timed {
+  int kind;
+  cudaEvent_t a, b;
+  uint64_t bytes;
+};
+
+struct Shard {
+  int device = 0;
+  int rank = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  double2* state = nullptr;
+  double2* scratch = nullptr;        // swap receive buffer
+  ncclComm_t comm = nullptr;
+  unsigned char* arena = nullptr;    // pass descriptors (device)
+  size_t arena_cap = 0;
+  double2* subpool = nullptr;        // booster sub-states (device)
+  size_t subpool_cap = 0;            // amplitudes
+  double2* tmp = nullptr;            // readout gather buffer
+  size_t tmp_cap = 0;                // amplitudes
+  int8_t* dmap = nullptr;            // logical->physical map (device)
+  std::vector<Timed> timed;          // per-launch events of the last call
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+};
+
+}  // namespace
+
+struct qs_ctx {
+  int n = 0, n_ranks = 1, n_global = 0, nl = 0;
+  Mode mode = M_SINGLE;
+  std::vector<Shard> shards;
+  qs_config_t cfg;
+  std::vector<int> map;              // logical -> physical
+  bool pending = true;               // state not yet written: it is |basis>
+  uint64_t basis = 0;
+  bool poisoned = false;
+  std::string err;
+  qs_stats_t stats;
+  uint64_t launches = 0;
+  unsigned char* host_stage = nullptr;  // pinned staging for descriptors
+  size_t host_stage_cap = 0;
+  double* host_tmp = nullptr;           // pinned readout staging
+  size_t host_tmp_cap = 0;
+  bool timing = true;
+  // per kernel kind: launches, ms, algorithmic bytes (last call, shard 0..)
+  uint64_t k_count[KK_NUM];
+  double k_ms[KK_NUM];
+  uint64_t k_bytes[KK_NUM];
+};
+
+namespace {
+
+int set_err(qs_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+#define CU(call)                                                                  \
+  do {                                                                            \
+    cudaError_t e_ = (call);                                                      \
+    if (e_ != cudaSuccess) {                                                      \
+      ctx->poisoned = true;                                                       \
+      return set_err(ctx, QS_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    }                                                                             \
+  } while (0)
+
+#define NC(call)                                                                  \
+  do {                                                                            \
+    ncclResult_t r_ = (call);                                                     \
+    if (r_ != ncclSuccess) {                                                      \
+      ctx->poisoned = true;                                                       \
+      return set_err(ctx, QS_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+    }                                                                             \
+  } while (0)
+
+int log2i(int x) {
+  int l = 0;
+  while ((1 << l) < x) l++;
+  return ((1 << l) == x) ? l : -1;
+}
+
+cudaEvent_t get_event(Shard& s) {
+  if (s.ev_used == s.ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    s.ev_pool.push_back(e);
+  }
+  return s.ev_pool[s.ev_used++];
+}
+
+int alloc_shard_memory(qs_ctx* ctx, Shard& s) {
+  CU(cudaSetDevice(s.device));
+  const size_t bytes = (size_t)16 << ctx->nl;
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  size_t need = bytes * ((ctx->n_ranks > 1) ? 2 : 1);
+  if (ctx->mode == M_LOOPBACK) need = 0;  // checked once by the caller
+  if (need > fr) {
+    char b[200];
+    snprintf(b, sizeof b, "need %zu bytes on device %d, %zu free", need, s.device, fr);
+    return set_err(ctx, QS_ENOMEM, b);
+  }
+  if (cudaMalloc(&s.state, bytes) != cudaSuccess)
+    return set_err(ctx, QS_ENOMEM, "cudaMalloc state failed (" + std::to_string(bytes) + " B)");
+  if (ctx->n_ranks > 1 && cudaMalloc(&s.scratch, bytes) != cudaSuccess)
+    return set_err(ctx, QS_ENOMEM, "cudaMalloc swap buffer failed (" + std::to_string(bytes) + " B)");
+  CU(cudaMalloc(&s.dmap, 64));
+  CU(cudaEventCreate(&s.t0));
+  CU(cudaEventCreate(&s.t1));
+  return QS_OK;
+}
+
+void init_ctx(qs_ctx* ctx, int n, int n_ranks) {
+  ctx->n = n;
+  ctx->n_ranks = n_ranks;
+  ctx->n_global = log2i(n_ranks);
+  ctx->nl = n - ctx->n_global;
+  qs_default_config(&ctx->cfg);
+  ctx->map.resize(n);
+  for (int q = 0; q < n; q++) ctx->map[q] = q;
+  ctx->pending = true;
+  ctx->basis = 0;
+  memset(&ctx->stats, 0, sizeof ctx->stats);
+  memset(ctx->k_count, 0, sizeof ctx->k_count);
+  memset(ctx->k_ms, 0, sizeof ctx->k_ms);
+  memset(ctx->k_bytes, 0, sizeof ctx->k_bytes);
+}
+
+int check_dims(int n, int n_ranks, std::string& why) {
+  if (n < 1 || n > 40) { why = "n_qubits must be in [1, 40]"; return QS_EINVAL; }
+  const int g = log2i(n_ranks);
+  if (n_ranks < 1 || g < 0) { why = "rank count must be a power of two"; return QS_EINVAL; }
+  const int nl = n - g;
+  if (nl < 1 || nl < g) { why = "too few local qubits for this rank count"; return QS_EINVAL; }
+  return QS_OK;
+}
+
+int ensure_host_stage(qs_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->host_stage_cap) return QS_OK;
+  if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
+  size_t cap = std::max(bytes, (size_t)1 << 20);
+  CU(cudaMallocHost(&ctx->host_stage, cap));
+  ctx->host_stage_cap = cap;
+  return QS_OK;
+}
+
+// ----------------------------------------------------------------- swap
+// Exchange global positions gpos[i] with local positions lpos[i] = nl-j+i.
+// Piece s (top j local bits) of rank r goes to rank r with bits b_i := s_i,
+// landing at its piece u(r) (a pure relabel afterwards).
+int exec_swap(qs_ctx* ctx, const Step& st) {
+  const int j = st.j, nl = ctx->nl;
+  const size_t piece = (size_t)1 << (nl - j);          // amplitudes
+  const size_t pbytes = piece * sizeof(double2);
+  std::vector<int> b(j);
+  for (int i = 0; i < j; i++) b[i] = st.gpos[i] - nl;
+  auto u_of = [&](int r) {
+    int u = 0;
+    for (int i = 0; i < j; i++) u |= ((r >> b[i]) & 1) << i;
+    return u;
+  };
+  auto dest = [&](int r, int s) {
+    int d = r;
+    for (int i = 0; i < j; i++) d = (d & ~(1 << b[i])) | (((s >> i) & 1) << b[i]);
+    return d;
+  };
+  if (ctx->mode == M_LOOPBACK) {
+    Shard& s0 = ctx->shards[0];
+    CU(cudaSetDevice(s0.device));
+    for (Shard& sh : ctx->shards) {
+      const int r = sh.rank, ur = u_of(r);
+      for (int s = 0; s < (1 << j); s++) {
+        Shard& dst = ctx->shards[dest(r, s)];
+        CU(cudaMemcpyAsync(dst.scratch + (size_t)ur * piece, sh.state + (size_t)s * piece,
+                           pbytes, cudaMemcpyDeviceToDevice, s0.stream));
+      }
+    }
+  } else {
+    NC(ncclGroupStart());
+    for (Shard& sh : ctx->shards) {
+      const int r = sh.rank, ur = u_of(r);
+      for (int s = 0; s < (1 << j); s++) {
+        if (s == ur) continue;
+        const int d = dest(r, s);
+        NC(ncclSend(sh.state + (size_t)s * piece, 2 * piece, ncclDouble, d, sh.comm, sh.stream));
+        NC(ncclRecv(sh.scratch + (size_t)s * piece, 2 * piece, ncclDouble, d, sh.comm, sh.stream));
+      }
+    }
+    NC(ncclGroupEnd());
+    for (Shard& sh : ctx->shards) {
+      CU(cudaSetDevice(sh.device));
+      const int ur = u_of(sh.rank);
+      CU(cudaMemcpyAsync(sh.scratch + (size_t)ur * piece, sh.state + (size_t)ur * piece, pbytes,
+                         cudaMemcpyDeviceToDevice, sh.stream));
+    }
+  }
+  for (Shard& sh : ctx->shards) std::swap(sh.state, sh.scratch);
+  return QS_OK;
+}
+
+// -------------------------------------------------------------- execute
+int execute(qs_ctx* ctx, const Plan& plan) {
+  // sub-state pool
+  std::vector<size_t> sub_off(plan.subs.size() + 1, 0);
+  size_t sub_total = 0;
+  for (size_t i = 0; i < plan.subs.size(); i++) {
+    sub_off[i + 1] = sub_total;
+    sub_total += (size_t)1 << plan.subs[i].nq;
+  }
+  // encode all pass descriptors per shard
+  std::vector<std::vector<size_t>> blob_off(ctx->shards.size());
+  std::vector<std::vector<unsigned char>> blobs(ctx->shards.size());
+  for (size_t si = 0; si < ctx->shards.size(); si++) {
+    Shard& sh = ctx->shards[si];
+    CU(cudaSetDevice(sh.device));
+    if (sub_total > sh.subpool_cap) {
+      if (sh.subpool) cudaFree(sh.subpool);
+      CU(cudaMalloc(&sh.subpool, sub_total * sizeof(double2)));
+      sh.subpool_cap = sub_total;
+    }
+    std::vector<unsigned char>& all = blobs[si];
+    for (const Step& st : plan.steps) {
+      size_t off = (size_t)-1;
+      if (st.type == Step::PASS) {
+        std::vector<unsigned char> b;
+        std::string err;
+        const int rank = (st.pass.buf == 0) ? sh.rank : 0;
+        int rc = encode_pass(st.pass, rank, b, err);
+        if (rc) return set_err(ctx, rc, err);
+        KPass h;
+        memcpy(&h, b.data(), sizeof h);
+        if (st.pass.src_mode == 1) {
+          h.expand.n = (int)st.pass.exp_bufs.size();
+          for (int g = 0; g < h.expand.n; g++) {
+            h.expand.ptr[g] = (u64)(sh.subpool + sub_off[st.pass.exp_bufs[g]]);
+            h.expand.lo[g] = st.pass.exp_lo[g];
+            h.expand.len[g] = st.pass.exp_len[g];
+          }
+          memcpy(b.data(), &h, sizeof h);
+        }
+        while (all.size() % 256) all.push_back(0);
+        off = all.size();
+        all.insert(all.end(), b.begin(), b.end());
+      }
+      blob_off[si].push_back(off);
+    }
+    if (all.size() > sh.arena_cap) {
+      if (sh.arena) cudaFree(sh.arena);
+      size_t cap = std::max(all.size() * 2, (size_t)1 << 20);
+      CU(cudaMalloc(&sh.arena, cap));
+      sh.arena_cap = cap;
+    }
+  }
+  size_t stage_total = 0;
+  for (auto& b : blobs) stage_total += (b.size() + 255) & ~(size_t)255;
+  int rc = ensure_host_stage(ctx, stage_total);
+  if (rc) return rc;
+  {
+    size_t o = 0;
+    for (size_t si = 0; si < ctx->shards.size(); si++) {
+      Shard& sh = ctx->shards[si];
+      if (blobs[si].empty()) continue;
+      memcpy(ctx->host_stage + o, blobs[si].data(), blobs[si].size());
+      CU(cudaSetDevice(sh.device));
+      CU(cudaMemcpyAsync(sh.arena, ctx->host_stage + o, blobs[si].size(),
+                         cudaMemcpyHostToDevice, sh.stream));
+      o += (blobs[si].size() + 255) & ~(size_t)255;
+    }
+  }
+  for (Shard& sh : ctx->shards) {
+    CU(cudaSetDevice(sh.device));
+    sh.timed.clear();
+    sh.ev_used = 0;
+    CU(cudaEventRecord(sh.t0, sh.stream));
+  }
+  const size_t shard_amps = (size_t)1 << ctx->nl;
+  for (size_t k = 0; k < plan.steps.size(); k++) {
+    const Step& st = plan.steps[k];
+    if (st.type == Step::SWAP) {
+      Shard& s0 = ctx->shards[0];
+      cudaEvent_t a = nullptr, b = nullptr;
+      if (ctx->timing) {
+        CU(cudaSetDevice(s0.device));
+        a = get_event(s0);
+        b = get_event(s0);
+        CU(cudaEventRecord(a, s0.stream));
+      }
+      rc = exec_swap(ctx, st);
+      if (rc) return rc;
+      if (ctx->timing) {
+        CU(cudaSetDevice(s0.device));
+        CU(cudaEventRecord(b, s0.stream));
+        s0.timed.push_back({KK_SWAP, a, b, (uint64_t)((16ull << ctx->nl) - (16ull << (ctx->nl - st.j)))});
+      }
+      continue;
+    }
+    for (size_t si = 0; si < ctx->shards.size(); si++) {
+      Shard& sh = ctx->shards[si];
+      CU(cudaSetDevice(sh.device));
+      cudaEvent_t a = nullptr, b = nullptr;
+      const bool tm = ctx->timing;
+      if (tm) {
+        a = get_event(sh);
+        b = get_event(sh);
+        CU(cudaEventRecord(a, sh.stream));
+      }
+      int kind = KK_INIT;
+      uint64_t bytes = 0;
+      switch (st.type) {
+        case Step::INIT_BASIS: {
+          CU(cudaMemsetAsync(sh.state, 0, shard_amps * sizeof(double2), sh.stream));
+          ctx->launches++;
+          if ((st.basis >> ctx->nl) == (u64)sh.rank) {
+            CU(launch_set_one(sh.state, st.basis & (shard_amps - 1), sh.stream));
+            ctx->launches++;
+          }
+          kind = KK_INIT;
+          bytes = 16ull << ctx->nl;
+          break;
+        }
+        case Step::SUB_INIT: {
+          double2* d = sh.subpool + sub_off[st.buf];
+          const size_t na = (size_t)1 << plan.subs[st.buf - 1].nq;
+          CU(cudaMemsetAsync(d, 0, na * sizeof(double2), sh.stream));
+          CU(launch_set_one(d, st.basis, sh.stream));
+          ctx->launches += 2;
+          kind = KK_INIT;
+          bytes = 16ull * na;
+          break;
+        }
+        case Step::SUB_MERGE: {
+          double2* d = sh.subpool + sub_off[st.buf];
+          const int la = plan.subs[st.src_a - 1].nq, lb = plan.subs[st.src_b - 1].nq;
+          CU(launch_merge(d, sh.subpool + sub_off[st.src_a], la, sh.subpool + sub_off[st.src_b], lb,
+                          sh.stream));
+          ctx->launches++;
+          kind = KK_MERGE;
+          bytes = 16ull << (la + lb);
+          break;
+        }
+        case Step::PERMUTE: {
+          CU(launch_permute(sh.state, sh.scratch, shard_amps, st.gpos.data(), st.lpos.data(),
+                            (int)st.gpos.size(), sh.stream));
+          std::swap(sh.state, sh.scratch);
+          ctx->launches++;
+          kind = KK_SWAP;
+          bytes = 32ull << ctx->nl;
+          break;
+        }
+        case Step::EXPAND: {
+          KExpand e;
+          memset(&e, 0, sizeof e);
+          e.n = (int)st.exp_bufs.size();
+          for (int g = 0; g < e.n; g++) {
+            e.ptr[g] = (u64)(sh.subpool + sub_off[st.exp_bufs[g]]);
+            e.lo[g] = st.exp_lo[g];
+            e.len[g] = st.exp_len[g];
+          }
+          CU(launch_expand(sh.state, shard_amps, (u64)sh.rank << ctx->nl, e, sh.stream));
+          ctx->launches++;
+          kind = KK_EXPAND;
+          bytes = 16ull << ctx->nl;
+          break;
+        }
+        case Step::PASS: {
+          const PassPlan& p = st.pass;
+          const unsigned char* dblob = sh.arena + blob_off[si][k];
+          KPass h;
+          memcpy(&h, blobs[si].data() + blob_off[si][k], sizeof h);
+          double2* buf = (p.buf == 0) ? sh.state : (sh.subpool + sub_off[p.buf]);
+          CU(launch_pass(p.kernel, dblob, h, buf, sh.stream));
+          ctx->launches++;
+          kind = p.kernel;
+          bytes = ((p.src_mode ? 16ull : 32ull) << p.nl);
+          break;
+        }
+        default:
+          break;
+      }
+      if (tm) {
+        CU(cudaEventRecord(b, sh.stream));
+        sh.timed.push_back({kind, a, b, bytes});
+      }
+    }
+  }
+  for (Shard& sh : ctx->shards) {
+    CU(cudaSetDevice(sh.device));
+    CU(cudaEventRecord(sh.t1, sh.stream));
+  }
+  for (Shard& sh : ctx->shards) {
+    CU(cudaSetDevice(sh.device));
+    CU(cudaStreamSynchronize(sh.stream));
+    CU(cudaGetLastError());
+  }
+  // timing
+  double tdev = 0;
+  for (Shard& sh : ctx->shards) {
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, sh.t0, sh.t1));
+    if (ms > tdev) tdev = ms;
+  }
+  ctx->stats.t_device_ms = tdev;
+  memset(ctx->k_count, 0, sizeof ctx->k_count);
+  memset(ctx->k_ms, 0, sizeof ctx->k_ms);
+  memset(ctx->k_bytes, 0, sizeof ctx->k_bytes);
+  double tswap = 0;
+  if (ctx->timing) {
+    Shard& s0 = ctx->shards[0];
+    for (const Timed& t : s0.timed) {
+      float ms = 0;
+      CU(cudaEventElapsedTime(&ms, t.a, t.b));
+      ctx->k_count[t.kind]++;
+      ctx->k_ms[t.kind] += ms;
+      ctx->k_bytes[t.kind] += t.bytes;
+      if (t.kind == KK_SWAP) tswap += ms;
+    }
+  }
+  ctx->stats.t_swap_ms = tswap;
+  return QS_OK;
+}
+
+int materialize(qs_ctx* ctx) {
+  if (!ctx->pending) return QS_OK;
+  return qs_apply_circuit(ctx, nullptr, 0);
+}
+
+}  // namespace
+
+// =================================================================== C-ABI
+extern "C" {
+
+void qs_default_config(qs_config_t* cfg) {
+  cfg->chunk_qubits = kChunkBits;
+  cfg->fuse_cap = 4;
+  cfg->diag_cap = 0;
+  cfg->boost_div = 2;
+  cfg->flags = QS_OPT_ALL;
+}
+
+static int create_common(qs_ctx* ctx) {
+  for (Shard& s : ctx->shards) {
+    int rc = alloc_shard_memory(ctx, s);
+    if (rc) return rc;
+  }
+  return QS_OK;
+}
+
+int qs_create(int n_qubits, int n_gpus, qs_ctx** out) {
+  if (!out) return QS_EINVAL;
+  *out = nullptr;
+  std::string why;
+  if (check_dims(n_qubits, n_gpus, why)) return QS_EINVAL;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return QS_ECUDA;
+  if (n_gpus > ndev) return QS_EINVAL;
+  qs_ctx* ctx = new qs_ctx();
+  *out = ctx;
+  init_ctx(ctx, n_qubits, n_gpus);
+  ctx->mode = M_SINGLE;
+  ctx->shards.resize(n_gpus);
+  for (int r = 0; r < n_gpus; r++) {
+    Shard& s = ctx->shards[r];
+    s.device = r;
+    s.rank = r;
+    CU(cudaSetDevice(r));
+    CU(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+    s.own_stream = true;
+  }
+  if (n_gpus > 1) {
+    std::vector<ncclComm_t> comms(n_gpus);
+    std::vector<int> devs(n_gpus);
+    for (int r = 0; r < n_gpus; r++) devs[r] = r;
+    NC(ncclCommInitAll(comms.data(), n_gpus, devs.data()));
+    for (int r = 0; r < n_gpus; r++) ctx->shards[r].comm = comms[r];
+  }
+  int rc = create_common(ctx);
+  if (rc) return rc;
+  return QS_OK;
+}
+
+int qs_create_loopback(int n_qubits, int n_ranks, int device, qs_ctx** out) {
+  if (!out) return QS_EINVAL;
+  *out = nullptr;
+  std::string why;
+  if (check_dims(n_qubits, n_ranks, why)) return QS_EINVAL;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return QS_ECUDA;
+  if (device < 0 || device >= ndev) return QS_EINVAL;
+  qs_ctx* ctx = new qs_ctx();
+  *out = ctx;
+  init_ctx(ctx, n_qubits, n_ranks);
+  ctx->mode = M_LOOPBACK;
+  ctx->shards.resize(n_ranks);
+  CU(cudaSetDevice(device));
+  cudaStream_t st;
+  CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  for (int r = 0; r < n_ranks; r++) {
+    Shard& s = ctx->shards[r];
+    s.device = device;
+    s.rank = r;
+    s.stream = st;
+    s.own_stream = (r == 0);
+  }
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  const size_t need = ((size_t)16 << ctx->nl) * 2 * n_ranks;
+  if (need > fr) return set_err(ctx, QS_ENOMEM, "loopback needs " + std::to_string(need) + " bytes");
+  return create_common(ctx);
+}
+
+int qs_nccl_unique_id(void* id_out_128) {
+  if (!id_out_128) return QS_EINVAL;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return QS_ENCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "nccl id size");
+  memcpy(id_out_128, &id, 128);
+  return QS_OK;
+}
+
+int qs_create_rank(int n_qubits, int world_size, int rank, int device, const void* nccl_id_128,
+                   qs_ctx** out) {
+  if (!out) return QS_EINVAL;
+  *out = nullptr;
+  std::string why;
+  if (check_dims(n_qubits, world_size, why)) return QS_EINVAL;
+  if (rank < 0 || rank >= world_size) return QS_EINVAL;
+  if (world_size > 1 && !nccl_id_128) return QS_EINVAL;
+  qs_ctx* ctx = new qs_ctx();
+  *out = ctx;
+  init_ctx(ctx, n_qubits, world_size);
+  ctx->mode = M_RANK;
+  ctx->shards.resize(1);
+  Shard& s = ctx->shards[0];
+  s.device = device;
+  s.rank = rank;
+  CU(cudaSetDevice(device));
+  CU(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+  s.own_stream = true;
+  if (world_size > 1) {
+    ncclUniqueId id;
+    memcpy(&id, nccl_id_128, 128);
+    NC(ncclCommInitRank(&s.comm, world_size, id, rank));
+  }
+  return create_common(ctx);
+}
+
+void qs_destroy(qs_ctx* ctx) {
+  if (!ctx) return;
+  for (Shard& s : ctx->shards) {
+    cudaSetDevice(s.device);
+    if (s.stream) cudaStreamSynchronize(s.stream);
+    if (s.comm) ncclCommDestroy(s.comm);
+    cudaFree(s.state);
+    cudaFree(s.scratch);
+    cudaFree(s.arena);
+    cudaFree(s.subpool);
+    cudaFree(s.tmp);
+    cudaFree(s.dmap);
+    for (cudaEvent_t e : s.ev_pool) cudaEventDestroy(e);
+    if (s.t0) cudaEventDestroy(s.t0);
+    if (s.t1) cudaEventDestroy(s.t1);
+    if (s.own_stream && s.stream) cudaStreamDestroy(s.stream);
+  }
+  if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
+  if (ctx->host_tmp) cudaFreeHost(ctx->host_tmp);
+  delete ctx;
+}
+
+int qs_set_config(qs_ctx* ctx, const qs_config_t* cfg) {
+  if (!ctx || !cfg) return QS_EINVAL;
+  if (cfg->chunk_qubits != kChunkBits)
+    return set_err(ctx, QS_EINVAL, "chunk_qubits must be 12 in this build");
+  if (cfg->fuse_cap < 1 || cfg->fuse_cap > 4) return set_err(ctx, QS_EINVAL, "fuse_cap in [1,4]");
+  if (cfg->diag_cap < 0 || cfg->diag_cap > 64) return set_err(ctx, QS_EINVAL, "diag_cap in [0,64]");
+  if (cfg->boost_div < 1 || cfg->boost_div > 64) return set_err(ctx, QS_EINVAL, "boost_div in [1,64]");
+  if (cfg->flags & ~QS_OPT_ALL) return set_err(ctx, QS_EINVAL, "unknown flags");
+  ctx->cfg = *cfg;
+  return QS_OK;
+}
+
+int qs_get_config(const qs_ctx* ctx, qs_config_t* cfg) {
+  if (!ctx || !cfg) return QS_EINVAL;
+  *cfg = ctx->cfg;
+  return QS_OK;
+}
+
+int qs_set_basis_state(qs_ctx* ctx, uint64_t x) {
+  if (!ctx) return QS_EINVAL;
+  if (ctx->poisoned) return QS_EPOISONED;
+  if (ctx->n < 64 && (x >> ctx->n)) return set_err(ctx, QS_EINVAL, "basis index >= 2^n");
+  ctx->pending = true;
+  ctx->basis = x;
+  for (int q = 0; q < ctx->n; q++) ctx->map[q] = q;
+  return QS_OK;
+}
+
+int qs_apply_circuit(qs_ctx* ctx, const qs_gate_t* gates, size_t n_gates) {
+  if (!ctx) return QS_EINVAL;
+  if (ctx->poisoned) return set_err(ctx, QS_EPOISONED, "handle poisoned by an earlier device error");
+  if (n_gates && !gates) return set_err(ctx, QS_EINVAL, "gates == NULL");
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<IrGate> ir;
+  std::string err;
+  int rc = ingest(ctx->n, gates, n_gates, ir, err);
+  if (rc) return set_err(ctx, rc, err);
+  PlanInput in;
+  in.n = ctx->n;
+  in.n_global = ctx->n_global;
+  in.cfg = ctx->cfg;
+  in.product_state = ctx->pending;
+  in.basis = ctx->basis;
+  in.map = ctx->map;
+  Plan plan;
+  rc = make_plan(in, ir, plan, err);
+  if (rc) return set_err(ctx, rc, err);
+  auto t1 = std::chrono::steady_clock::now();
+  ctx->launches = 0;
+  rc = execute(ctx, plan);
+  if (rc) return rc;
+  ctx->map = plan.map_out;
+  ctx->pending = false;
+  qs_stats_t& s = ctx->stats;
+  const PlanStats& ps = plan.stats;
+  s.n_gates_in = ps.n_gates_in;
+  s.n_passes = ps.n_passes;
+  s.n_chunk_passes = ps.n_chunk;
+  s.n_dense_passes = ps.n_dense;
+  s.n_diag_passes = ps.n_diag;
+  s.n_small_passes = ps.n_small;
+  s.n_expand = ps.n_expand;
+  s.n_swaps = ps.n_swaps;
+  s.n_substate_gates = ps.n_sub_gates;
+  s.n_fused_diag = ps.n_fused_diag;
+  s.bytes_hbm = ps.bytes_hbm;
+  s.bytes_nvlink = ps.bytes_nvlink;
+  s.paper_updates = ps.paper_updates;
+  s.naive_updates = ps.naive_updates;
+  s.t_plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  return QS_OK;
+}
+
+static int readout(qs_ctx* ctx, double* host_out, uint64_t offset, uint64_t count, int probs) {
+  if (!ctx || (!host_out && count)) return QS_EINVAL;
+  if (ctx->poisoned) return set_err(ctx, QS_EPOISONED, "handle poisoned");
+  const uint64_t total = (ctx->n >= 64) ? ~0ull : (1ull << ctx->n);
+  if (offset > total || count > total - offset) return set_err(ctx, QS_EINVAL, "range exceeds 2^n");
+  int rc = materialize(ctx);
+  if (rc) return rc;
+  const int per = probs ? 1 : 2;
+  const uint64_t slice = (uint64_t)1 << 22;
+  const size_t need_host = (size_t)std::min<uint64_t>(slice, std::max<uint64_t>(count, 1)) * 2;
+  if (ctx->host_tmp_cap < need_host) {
+    if (ctx->host_tmp) cudaFreeHost(ctx->host_tmp);
+    CU(cudaMallocHost(&ctx->host_tmp, need_host * sizeof(double)));
+    ctx->host_tmp_cap = need_host;
+  }
+  int8_t hmap[64];
+  memset(hmap, 0, sizeof hmap);
+  for (int q = 0; q < ctx->n; q++) hmap[q] = (int8_t)ctx->map[q];
+  for (Shard& sh : ctx->shards) {
+    CU(cudaSetDevice(sh.device));
+    if (sh.tmp_cap < slice) {
+      if (sh.tmp) cudaFree(sh.tmp);
+      CU(cudaMalloc(&sh.tmp, slice * sizeof(double2)));
+      sh.tmp_cap = slice;
+    }
+    CU(cudaMemcpyAsync(sh.dmap, hmap, 64, cudaMemcpyHostToDevice, sh.stream));
+  }
+  memset(host_out, 0, count * per * sizeof(double));
+  for (uint64_t done = 0; done < count; done += slice) {
+    const uint64_t c = std::min(slice, count - done);
+    if (ctx->mode == M_RANK) {
+      Shard& sh = ctx->shards[0];
+      CU(cudaSetDevice(sh.device));
+      CU(launch_gather(sh.state, sh.tmp, offset + done, c, ctx->n, sh.dmap, ctx->nl,
+                       (u64)sh.rank, probs, sh.stream));
+      if (ctx->n_ranks > 1)
+        NC(ncclAllReduce(sh.tmp, sh.tmp, c * per, ncclDouble, ncclSum, sh.comm, sh.stream));
+      CU(cudaMemcpyAsync(ctx->host_tmp, sh.tmp, c * per * sizeof(double), cudaMemcpyDeviceToHost,
+                         sh.stream));
+      CU(cudaStreamSynchronize(sh.stream));
+      memcpy(host_out + done * per, ctx->host_tmp, c * per * sizeof(double));
+    } else {
+      for (Shard& sh : ctx->shards) {
+        CU(cudaSetDevice(sh.device));
+        CU(launch_gather(sh.state, sh.tmp, offset + done, c, ctx->n, sh.dmap, ctx->nl,
+                         (u64)sh.rank, probs, sh.stream));
+        CU(cudaMemcpyAsync(ctx->host_tmp, sh.tmp, c * per * sizeof(double),
+                           cudaMemcpyDeviceToHost, sh.stream));
+        CU(cudaStreamSynchronize(sh.stream));
+        double* o = host_out + done * per;
+        for (uint64_t i = 0; i < c * per; i++) o[i] += ctx->host_tmp[i];
+      }
+    }
+  }
+  return QS_OK;
+}
+
+int qs_get_state(qs_ctx* ctx, double* host_out, uint64_t offset, uint64_t count) {
+  return readout(ctx, host_out, offset, count, 0);
+}
+
+int qs_probabilities(qs_ctx* ctx, double* host_out, uint64_t offset, uint64_t count) {
+  return readout(ctx, host_out, offset, count, 1);
+}
+
+int qs_get_stats(const qs_ctx* ctx, qs_stats_t* out) {
+  if (!ctx || !out) return QS_EINVAL;
+  *out = ctx->stats;
+  return QS_OK;
+}
+
+const char* qs_last_error(const qs_ctx* ctx) { return ctx ? ctx->err.c_str() : "NULL handle"; }
+
+int64_t qs_plan_json(int n_qubits, int n_ranks, const qs_config_t* cfg, int product_state,
+                     uint64_t basis, const qs_gate_t* gates, size_t n_gates, int detail,
+                     char* buf, size_t cap) {
+  std::string err;
+  auto fail = [&](int rc) -> int64_t {
+    if (buf && cap) {
+      size_t k = std::min(cap - 1, err.size());
+      memcpy(buf, err.data(), k);
+      buf[k] = 0;
+    }
+    return rc;
+  };
+  if (check_dims(n_qubits, n_ranks, err)) return fail(QS_EINVAL);
+  std::vector<IrGate> ir;
+  int rc = ingest(n_qubits, gates, n_gates, ir, err);
+  if (rc) return fail(rc);
+  PlanInput in;
+  in.n = n_qubits;
+  in.n_global = log2i(n_ranks);
+  if (cfg) in.cfg = *cfg;
+  else qs_default_config(&in.cfg);
+  in.product_state = product_state != 0;
+  in.basis = basis;
+  in.map.resize(n_qubits);
+  for (int q = 0; q < n_qubits; q++) in.map[q] = q;
+  Plan plan;
+  rc = make_plan(in, ir, plan, err);
+  if (rc) return fail(rc);
+  // also validate that every pass encodes
+  for (const Step& st : plan.steps)
+    if (st.type == Step::PASS) {
+      std::vector<unsigned char> b;
+      rc = encode_pass(st.pass, 0, b, err);
+      if (rc) return fail(rc);
+    }
+  std::string js = plan_to_json(plan, detail != 0);
+  if (buf && cap) {
+    size_t k = std::min(cap - 1, js.size());
+    memcpy(buf, js.data(), k);
+    buf[k] = 0;
+  }
+  return (int64_t)js.size();
+}
+
+int qs_divider(int n, int div_size, int* out, int cap) {
+  if (n < 1 || div_size < 1 || !out) return QS_EINVAL;
+  std::vector<int> q;
+  divider(n, div_size, q);
+  if ((int)q.size() > cap) return QS_EINVAL;
+  for (size_t i = 0; i < q.size(); i++) out[i] = q[i];
+  return (int)q.size();
+}
+
+uint64_t qs_last_launches(const qs_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+void* qs_get_stream(const qs_ctx* ctx, int i) {
+  if (!ctx || i < 0 || i >= (int)ctx->shards.size()) return nullptr;
+  return (void*)ctx->shards[i].stream;
+}
+
+int qs_set_timing(qs_ctx* ctx, int enable) {
+  if (!ctx) return QS_EINVAL;
+  ctx->timing = enable != 0;
+  return QS_OK;
+}
+
+int qs_get_kernel_timing(const qs_ctx* ctx, int kind, uint64_t* launches, double* ms,
+                         uint64_t* bytes) {
+  if (!ctx || kind < 0 || kind >= KK_NUM) return QS_EINVAL;
+  if (launches) *launches = ctx->k_count[kind];
+  if (ms) *ms = ctx->k_ms[kind];
+  if (bytes) *bytes = ctx->k_bytes[kind];
+  return QS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,1072 @@
+// planner.cpp -- host optimiser: Alg. 4 "Swarm optimization" (PAPER.md
+// L391-416) re-designed for B200.
+//
+//   Booster            Alg. 6/7 with readings c8-c11.
+//   DiagonalDetector   Alg. 8 with corrections c4-c7.
+//   GBSA rank level stages whose non-diagonal targets are local;
+//                      global<->local swaps between stages.
+//   GBSA machine level cache blocking into chunk passes: every
+//                      non-diagonal target of a pass lies in the pass's 12
+//                      chunk positions; diagonals and controls need no
+//                      locality (evaluated from index bits, incl. rank bits).
+//   GBSA fuse=1 cost-based fusion of adjacent dense ops
+//                      (FP64-FMA cost model, reading c15).
+//   Virtual qubit map  logical -> physical; uncontrolled SWAPs are relabels
+//                      (Eq. 4).
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <sstream>
+
+#include "planner.hpp"
+
+namespace qs {
+
+static inline int popc(u64 x) { return __builtin_popcountll(x); }
+
+// ------------------------------------------------------------ Alg. 6
+void divider(int n, int div_size, std::vector<int>& que) {
+  if (n <= div_size) {
+    que.push_back(n);
+    return;
+  }
+  divider(n >> 1, div_size, que);
+  n = (n & 1) ? n + 1 : n;
+  divider(n >> 1, div_size, que);
+}
+
+// ------------------------------------------------------------ helpers
+static void merge_mono(std::vector<Mono>& m) {
+  std::sort(m.begin(), m.end(), [](const Mono& a, const Mono& b) { return a.mask < b.mask; });
+  std::vector<Mono> out;
+  for (const Mono& x : m) {
+    if (!out.empty() && out.back().mask == x.mask) out.back().coeff += x.coeff;
+    else out.push_back(x);
+  }
+  m.clear();
+  for (const Mono& x : out)
+    if (x.coeff != 0) m.push_back(x);
+}
+
+static u64 map_mask(u64 logical_mask, const std::vector<int>& map) {
+  u64 r = 0;
+  while (logical_mask) {
+    int q = __builtin_ctzll(logical_mask);
+    logical_mask &= logical_mask - 1;
+    r |= 1ull << map[q];
+  }
+  return r;
+}
+
+// Matrix product C = A * B for gates given over target lists; result over
+// `uni` (ascending union).  Matrix bit i <-> targets[i].
+static std::vector<cd> embed(const std::vector<cd>& m, const std::vector<int>& tg,
+                             const std::vector<int>& uni) {
+  const int t = (int)tg.size(), u = (int)uni.size();
+  const int D = 1 << u, d = 1 << t;
+  std::vector<int> idx(t);
+  for (int i = 0; i < t; i++)
+    idx[i] = (int)(std::find(uni.begin(), uni.end(), tg[i]) - uni.begin());
+  std::vector<cd> out((size_t)D * D, 0);
+  for (int r = 0; r < D; r++)
+    for (int c = 0; c < D; c++) {
+      // identity on the non-target bits
+      int rest_r = r, rest_c = c, sr = 0, sc = 0;
+      for (int i = 0; i < t; i++) {
+        sr |= ((r >> idx[i]) & 1) << i;
+        sc |= ((c >> idx[i]) & 1) << i;
+        rest_r &= ~(1 << idx[i]);
+        rest_c &= ~(1 << idx[i]);
+      }
+      if (rest_r != rest_c) continue;
+      out[(size_t)r * D + c] = m[(size_t)sr * d + sc];
+    }
+  return out;
+}
+
+static std::vector<cd> matmul(const std::vector<cd>& A, const std::vector<cd>& B, int D) {
+  std::vector<cd> C((size_t)D * D, 0);
+  for (int i = 0; i < D; i++)
+    for (int k = 0; k < D; k++) {
+      cd a = A[(size_t)i * D + k];
+      if (a == cd(0, 0)) continue;
+      for (int j = 0; j < D; j++) C[(size_t)i * D + j] += a * B[(size_t)k * D + j];
+    }
+  return C;
+}
+
+// ------------------------------------------------------------ Alg. 8
+// Corrected diagonal detector (readings c4-c7):
+//  c4  dependencies use the support (targets U controls);
+//  c5  a non-diagonal is deferred (uList, stopTable) when its support meets
+//      depSet OR a stopTable-marked qubit, else bypassed ahead of the fusion;
+//  c6  a lone diagonal is kept (the printed Alg. 8 drops it);
+//  c7  a diagonal touching a stopTable-marked qubit stops the scan; so does
+//      exceeding the D cap on the fused support (diag_cap > 0).
+std::vector<IrGate> diagonal_detector(const std::vector<IrGate>& in, int n, int diag_cap,
+                                      uint64_t* n_fused) {
+  (void)n;
+  std::vector<IrGate> res;           // resList
+  res.reserve(in.size());
+  size_t it = 0;
+  while (it < in.size()) {
+    if (in[it].type != IrGate::DIAG) {
+      res.push_back(in[it]);
+      ++it;
+      continue;
+    }
+    IrGate fused = in[it];             // diagList (merged as we go)
+    std::vector<IrGate> ulist;         // uList
+    u64 stop = 0;                      // stopTable
+    u64 dep = in[it].support;          // depSet
+    int diag_size = 1;
+    size_t f = it + 1;
+    for (; f < in.size(); ++f) {
+      const IrGate& g = in[f];
+      const u64 s = g.support;
+      if (g.type != IrGate::DIAG) {
+        if (s & (dep | stop)) {        // c5
+          stop |= s;
+          ulist.push_back(g);
+        } else {
+          res.push_back(g);
+        }
+      } else {
+        if (s & stop) break;           // checkStop (c7)
+        if (diag_cap > 0 && popc(dep | s) > diag_cap) break;
+        dep |= s;
+        fused.mono.insert(fused.mono.end(), g.mono.begin(), g.mono.end());
+        fused.support |= s;
+        fused.n_src += g.n_src;
+        ++diag_size;
+      }
+    }
+    if (diag_size > 1) {               // doDiagonalFusion
+      merge_mono(fused.mono);
+      fused.kind = -1;
+      if (n_fused) ++*n_fused;
+    }
+    res.push_back(std::move(fused));   // c6: singletons are kept
+    for (auto& g : ulist) res.push_back(std::move(g));
+    it = f;
+  }
+  return res;
+}
+
+// ------------------------------------------------------------ scheduling
+struct Sched {
+  Plan* plan;
+  const qs_config_t* cfg;
+  int src_mode = 0;                 // pending source of the next main pass: 0 none,
+                                    // 1 expand (booster), 2 basis
+  std::vector<int> exp_bufs, exp_lo, exp_len;
+  uint64_t basis_phys = 0;
+};
+
+static double dense_cost(int k) { return 4.0 * (1 << k); }  // FP64 FMA per amp
+
+// Emit the pending source as a standalone step (before a swap / small pass).
+static void flush_source(Sched& S) {
+  if (S.src_mode == 1) {
+    Step st;
+    st.type = Step::EXPAND;
+    st.buf = 0;
+    st.exp_bufs = S.exp_bufs;
+    st.exp_lo = S.exp_lo;
+    st.exp_len = S.exp_len;
+    S.plan->steps.push_back(st);
+    S.plan->stats.n_expand++;
+    S.plan->stats.bytes_hbm += (16ull << S.plan->nl);
+  } else if (S.src_mode == 2) {
+    Step st;
+    st.type = Step::INIT_BASIS;
+    st.buf = 0;
+    st.basis = S.basis_phys;
+    S.plan->steps.push_back(st);
+    S.plan->stats.bytes_hbm += (16ull << S.plan->nl);
+  }
+  S.src_mode = 0;
+}
+
+static POp dense_pop(const IrGate& g, const std::vector<int>& map) {
+  POp op;
+  op.type = POp::DENSE;
+  for (int q : g.targets) op.tpos.push_back(map[q]);
+  u64 cm = 0;
+  for (int q : g.controls) cm |= 1ull << map[q];
+  op.cmask = cm;
+  op.mat = g.mat;
+  op.is_h = g.is_h;
+  op.is_x = g.is_x;
+  op.n_src = g.n_src;
+  return op;
+}
+
+static void add_diag_op(std::vector<POp>& ops, const IrGate& g, const std::vector<int>& map) {
+  if (ops.empty() || ops.back().type != POp::DIAG) {
+    POp op;
+    op.type = POp::DIAG;
+    op.n_src = 0;
+    ops.push_back(op);
+  }
+  POp& d = ops.back();
+  for (const Mono& m : g.mono) d.mono.push_back({map_mask(m.mask, map), m.coeff});
+  d.n_src += g.n_src;
+}
+
+// GBSA fuse=1: fuse adjacent uncontrolled dense ops when the fused
+// gate's FP64 cost does not exceed the sum of the parts (reading c15).
+static void fuse_ops(std::vector<POp>& ops, int fuse_cap) {
+  if (fuse_cap < 2) return;
+  std::vector<POp> out;
+  for (POp& op : ops) {
+    if (!out.empty() && op.type == POp::DENSE && out.back().type == POp::DENSE &&
+        op.cmask == 0 && out.back().cmask == 0) {
+      POp& prev = out.back();
+      std::vector<int> uni = prev.tpos;
+      for (int p : op.tpos)
+        if (std::find(uni.begin(), uni.end(), p) == uni.end()) uni.push_back(p);
+      std::sort(uni.begin(), uni.end());
+      const int ku = (int)uni.size();
+      const double fused = dense_cost(ku);
+      const double parts = (prev.is_h ? 2.0 : dense_cost((int)prev.tpos.size())) +
+                           (op.is_h ? 2.0 : dense_cost((int)op.tpos.size()));
+      if (ku <= std::min(fuse_cap, kRegBits - 1) && fused <= parts) {
+        std::vector<cd> A = embed(prev.mat, prev.tpos, uni);
+        std::vector<cd> B = embed(op.mat, op.tpos, uni);
+        prev.mat = matmul(B, A, 1 << ku);  // later gate applied after
+        prev.tpos = uni;
+        prev.is_h = prev.is_x = false;
+        prev.n_src += op.n_src;
+        continue;
+      }
+    }
+    out.push_back(std::move(op));
+  }
+  ops.swap(out);
+}
+
+// Assign register layouts ("phases") to the dense ops of a chunk pass.
+static void assign_phases(PassPlan& p) {
+  const int m = (int)p.cpos.size();
+  auto cbit = [&](int pos) {
+    return (int)(std::find(p.cpos.begin(), p.cpos.end(), pos) - p.cpos.begin());
+  };
+  p.phase_regs.clear();
+  p.op_phase.assign(p.ops.size(), 0);
+  std::vector<int> cur;
+  int ph = 0;
+  for (size_t i = 0; i < p.ops.size(); i++) {
+    const POp& op = p.ops[i];
+    if (op.type == POp::DENSE) {
+      std::vector<int> need;
+      for (int pos : op.tpos) need.push_back(cbit(pos));
+      std::vector<int> uni = cur;
+      for (int c : need)
+        if (std::find(uni.begin(), uni.end(), c) == uni.end()) uni.push_back(c);
+      if ((int)uni.size() > kRegBits) {
+        p.phase_regs.push_back(cur);
+        ++ph;
+        cur = need;
+      } else {
+        cur = uni;
+      }
+    }
+    p.op_phase[i] = ph;
+  }
+  p.phase_regs.push_back(cur);
+  // fill every layout to kRegBits register bits, preferring high chunk bits
+  for (auto& regs : p.phase_regs) {
+    for (int c = m - 1; c >= 0 && (int)regs.size() < kRegBits; c--)
+      if (std::find(regs.begin(), regs.end(), c) == regs.end()) regs.push_back(c);
+    std::sort(regs.begin(), regs.end());
+  }
+  if (p.kernel != KK_DIAG) p.kernel = (p.phase_regs.size() > 1) ? KK_CHUNK : KK_DENSE;
+}
+
+static void finalize_chunk_pass(Sched& S, PassPlan& p, u64 need_pos, int nl) {
+  const int m = kChunkBits;
+  // chunk positions: the needed ones, filled with the lowest free positions
+  u64 c = need_pos;
+  for (int pos = 0; pos < nl && popc(c) < m; pos++) c |= 1ull << pos;
+  p.cpos.clear();
+  for (int pos = 0; pos < nl; pos++)
+    if (c >> pos & 1) p.cpos.push_back(pos);
+  p.opos = p.cpos;
+  for (POp& op : p.ops)
+    if (op.type == POp::DIAG) merge_mono(op.mono);
+  bool all_diag = true;
+  for (const POp& op : p.ops)
+    if (op.type != POp::DIAG) all_diag = false;
+  p.kernel = all_diag ? KK_DIAG : KK_CHUNK;
+  fuse_ops(p.ops, (S.cfg->flags & QS_OPT_FUSE) ? S.cfg->fuse_cap : 1);
+  assign_phases(p);
+  if (S.src_mode && p.buf == 0) {
+    p.src_mode = S.src_mode;
+    p.exp_bufs = S.exp_bufs;
+    p.exp_lo = S.exp_lo;
+    p.exp_len = S.exp_len;
+    p.basis = S.basis_phys;
+    S.src_mode = 0;
+  }
+}
+
+// Schedule `gates` (logical) on buffer `buf` (nq qubits of which nl local,
+// map logical->physical).  Appends steps; updates `map` (relabels, swaps).
+static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
+                    std::vector<IrGate> gates, std::string& err) {
+  Plan& plan = *S.plan;
+  const int n_global = nq - nl;
+  const bool blocking = (S.cfg->flags & QS_OPT_BLOCK) != 0;
+  const int l = 5;
+  std::vector<IrGate> rem = std::move(gates);
+  int guard = 0;
+  while (!rem.empty()) {
+    if (++guard > 1000000) {
+      err = "planner failed to make progress";
+      return QS_EINVAL;
+    }
+    PassPlan p;
+    p.buf = buf;
+    p.nl = nl;
+    p.n_global = n_global;
+    const bool small = nl <= kSmallMax;
+    u64 need = 0;
+    if (!small)
+      for (int i = 0; i < l; i++) need |= 1ull << i;
+    u64 blocked_all = 0, blocked_nd = 0;
+    std::vector<IrGate> deferred;
+    bool stop = false;
+    bool progress = false;
+    double cost = 0;
+    size_t n_mono = 0;
+    int dense_taken = 0;
+    for (size_t gi = 0; gi < rem.size(); gi++) {
+      IrGate& g = rem[gi];
+      const u64 s = g.support;
+      auto defer = [&]() {
+        blocked_all |= s;
+        if (g.type != IrGate::DIAG) blocked_nd |= s;
+        deferred.push_back(std::move(g));
+      };
+      if (stop) { defer(); continue; }
+      if (g.type == IrGate::RELABEL) {
+        if (s & blocked_all) { defer(); continue; }
+        std::swap(map[g.targets[0]], map[g.targets[1]]);
+        progress = true;
+        continue;
+      }
+      if (g.type == IrGate::DIAG) {
+        if (s & blocked_nd) { defer(); continue; }
+        if (!small && n_mono + g.mono.size() > 4000 && n_mono > 0) { stop = true; defer(); continue; }
+        if (p.ops.empty() || p.ops.back().type != POp::DIAG) cost += 24;
+        add_diag_op(p.ops, g, map);
+        n_mono += g.mono.size();
+        progress = true;
+        continue;
+      }
+      // DENSE
+      if (s & blocked_all) { defer(); continue; }
+      u64 tp = 0;
+      bool global = false;
+      for (int q : g.targets) {
+        if (map[q] >= nl) global = true;
+        tp |= 1ull << map[q];
+      }
+      if (global) { defer(); continue; }
+      if (!small) {
+        if ((int)g.targets.size() > kRegBits - 1) {
+          err = "dense gates with more than 3 targets need a state of <= 12 local qubits";
+          return QS_EUNSUPPORTED;
+        }
+        u64 nn = need | tp;
+        if (popc(nn) > kChunkBits) { defer(); continue; }
+        const double c = g.is_h ? 2.0 : dense_cost((int)g.targets.size());
+        if (cost + c > 200.0 && dense_taken > 0) { stop = true; defer(); continue; }
+        if (!blocking && dense_taken > 0) { stop = true; defer(); continue; }
+        need = nn;
+        cost += c;
+      }
+      p.ops.push_back(dense_pop(g, map));
+      ++dense_taken;
+      progress = true;
+    }
+    rem.swap(deferred);
+    if (!p.ops.empty()) {
+      if (small) {
+        if (S.src_mode && buf == 0) {
+          p.src_mode = S.src_mode;
+          p.exp_bufs = S.exp_bufs;
+          p.exp_lo = S.exp_lo;
+          p.exp_len = S.exp_len;
+          p.basis = S.basis_phys;
+          S.src_mode = 0;
+        }
+        p.kernel = KK_SMALL;
+        p.cpos.clear();
+      } else {
+        finalize_chunk_pass(S, p, need, nl);
+      }
+      plan.steps.push_back(Step{Step::PASS, p});
+      if (buf == 0) {  // statistics count full-state passes only
+        if (p.kernel == KK_CHUNK) plan.stats.n_chunk++;
+        else if (p.kernel == KK_DENSE) plan.stats.n_dense++;
+        else if (p.kernel == KK_DIAG) plan.stats.n_diag++;
+        else plan.stats.n_small++;
+        plan.stats.n_passes++;
+        plan.stats.bytes_hbm += ((p.src_mode ? 16ull : 32ull) << nl);
+      }
+      continue;
+    }
+    if (progress) continue;  // only relabels were taken
+    // Nothing applicable: the first pending dense gate has a global target.
+    if (n_global == 0) {
+      err = "internal: no progress on a single-rank buffer";
+      return QS_EINVAL;
+    }
+    // rem[0] is the blocked gate (a diagonal or relabel at the head would
+    // have been taken): bring its global targets in, keep its local targets,
+    // and bring further globals needed by later gates while room remains.
+    std::vector<int> gpos;
+    u64 protect = 0;
+    for (int q : rem[0].targets) {
+      if (map[q] >= nl) gpos.push_back(map[q]);
+      else protect |= 1ull << map[q];
+    }
+    for (const IrGate& g : rem) {
+      if (g.type != IrGate::DENSE) continue;
+      for (int q : g.targets)
+        if (map[q] >= nl && std::find(gpos.begin(), gpos.end(), map[q]) == gpos.end() &&
+            (int)gpos.size() < n_global && (int)gpos.size() + 1 + popc(protect) <= nl)
+          gpos.push_back(map[q]);
+      if ((int)gpos.size() == n_global) break;
+    }
+    std::sort(gpos.begin(), gpos.end());
+    const int j = (int)gpos.size();
+    if (j > nl) {
+      err = "too few local qubits for the swap";
+      return QS_EINVAL;
+    }
+    for (const IrGate& g : rem)
+      if (g.type == IrGate::DENSE && (int)g.targets.size() > nl) {
+        err = "a gate has more targets than there are local qubits";
+        return QS_EINVAL;
+      }
+    if (buf == 0) flush_source(S);
+    std::vector<int> inv(nq);
+    for (int q = 0; q < nq; q++) inv[map[q]] = q;
+    // Victims: the j local qubits whose next use as a dense target is the
+    // farthest (Belady), preferring those already at the top positions.
+    std::vector<size_t> next(nq, (size_t)-1);
+    for (size_t i = rem.size(); i-- > 0;)
+      if (rem[i].type == IrGate::DENSE)
+        for (int q : rem[i].targets) next[q] = i;
+    std::vector<int> cand;
+    for (int p = 0; p < nl; p++)
+      if (!(protect >> p & 1)) cand.push_back(p);
+    std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) {
+      const size_t na = next[inv[a]], nb = next[inv[b]];
+      if (na != nb) return na > nb;
+      return a > b;  // prefer high (top) positions
+    });
+    std::vector<int> victims(cand.begin(), cand.begin() + j);
+    std::vector<int> top;
+    for (int i = 0; i < j; i++) top.push_back(nl - j + i);
+    {
+      // local bit permutation bringing the victims to the top positions
+      std::vector<int> tv, vv;  // top non-victims, victims not on top
+      for (int t : top)
+        if (std::find(victims.begin(), victims.end(), t) == victims.end()) tv.push_back(t);
+      for (int v : victims)
+        if (v < nl - j) vv.push_back(v);
+      if (!tv.empty()) {
+        Step ps;
+        ps.type = Step::PERMUTE;
+        for (size_t i = 0; i < tv.size(); i++) {
+          ps.gpos.push_back(tv[i]);
+          ps.lpos.push_back(vv[i]);
+          std::swap(map[inv[tv[i]]], map[inv[vv[i]]]);
+          std::swap(inv[tv[i]], inv[vv[i]]);
+        }
+        plan.steps.push_back(ps);
+        plan.stats.n_passes++;
+        plan.stats.bytes_hbm += (32ull << nl);
+      }
+    }
+    Step st;
+    st.type = Step::SWAP;
+    st.j = j;
+    st.gpos = gpos;
+    st.lpos = top;
+    // relabel: logical at gpos[i] <-> logical at lpos[i]
+    for (int i = 0; i < j; i++) std::swap(map[inv[st.gpos[i]]], map[inv[st.lpos[i]]]);
+    plan.steps.push_back(st);
+    plan.stats.n_swaps++;
+    plan.stats.bytes_nvlink += (16ull << nl) - (16ull << (nl - j));
+  }
+  return QS_OK;
+}
+
+// ------------------------------------------------------------ Alg. 7
+// Merge booster (readings c8-c11).  Sub-state buffers are simulated with the
+// same scheduler (replicated on every rank); the final merge into the full
+// state is fused into the load of the first full-state pass (K5 as a source).
+static int booster(Sched& S, int n, std::vector<IrGate>& gates, std::string& err) {
+  Plan& plan = *S.plan;
+  const int B = std::max(1, S.cfg->boost_div);
+  std::vector<int> que;
+  divider(n, (n + B - 1) / B, que);
+  if (que.size() <= 1) return QS_OK;  // nothing to divide: plain basis source
+  struct Grp { int lo, len, buf; };
+  std::vector<Grp> groups;
+  int lo = 0;
+  auto new_sub = [&](int len, int glo) {
+    plan.subs.push_back(SubBuf{len, glo});
+    return (int)plan.subs.size();  // ids start at 1
+  };
+  for (int len : que) {
+    Grp g{lo, len, new_sub(len, lo)};
+    Step st;
+    st.type = Step::SUB_INIT;
+    st.buf = g.buf;
+    st.basis = (S.basis_phys >> lo) & ((1ull << len) - 1);
+    plan.steps.push_back(st);
+    groups.push_back(g);
+    lo += len;
+  }
+  uint64_t sub_gates = 0;
+  while (groups.size() > 1) {
+    std::vector<int> round_counts;
+    for (Grp& g : groups) {
+      const u64 gm = ((g.len >= 64) ? ~0ull : ((1ull << g.len) - 1)) << g.lo;
+      // genGateBlock (c11): support within the group and every earlier
+      // unscheduled gate overlapping it already scheduled.
+      std::vector<IrGate> mine, rest;
+      u64 blocked = 0;
+      for (IrGate& x : gates) {
+        if ((x.support & ~gm) == 0 && !(x.support & blocked)) {
+          mine.push_back(std::move(x));
+        } else {
+          blocked |= x.support;
+          rest.push_back(std::move(x));
+        }
+      }
+      gates.swap(rest);
+      round_counts.push_back((int)mine.size());
+      plan.stats.paper_updates += (uint64_t)mine.size() << g.len;
+      sub_gates += mine.size();
+      if (!mine.empty()) {
+        // remap to sub-state qubits; relabels become physical SWAPs here
+        for (IrGate& x : mine) {
+          if (x.type == IrGate::RELABEL) {
+            x.type = IrGate::DENSE;
+            int t = 0;
+            gate_matrix(QS_SWAP, nullptr, x.mat, &t);
+          }
+          for (int& q : x.targets) q -= g.lo;
+          for (int& q : x.controls) q -= g.lo;
+          x.support >>= g.lo;
+          for (Mono& mo : x.mono) mo.mask >>= g.lo;
+        }
+        std::vector<int> smap(g.len);
+        for (int i = 0; i < g.len; i++) smap[i] = i;
+        int rc = schedule(S, g.buf, g.len, g.len, smap, std::move(mine), err);
+        if (rc) return rc;
+      }
+    }
+    plan.stats.booster_rounds.push_back(round_counts);
+    // merge pairwise, c8: odd leftover kept as its own group
+    std::vector<Grp> next;
+    if (groups.size() == 2 && groups[0].len + groups[1].len == n) {
+      // final merge: fused into the first full-state pass (or standalone)
+      S.src_mode = 1;
+      S.exp_bufs.clear(); S.exp_lo.clear(); S.exp_len.clear();
+      for (Grp& g : groups) {
+        S.exp_bufs.push_back(g.buf);
+        S.exp_lo.push_back(g.lo);
+        S.exp_len.push_back(g.len);
+      }
+      plan.stats.paper_updates += 1ull << n;
+      groups.clear();
+      groups.push_back(Grp{0, n, 0});
+      break;
+    }
+    for (size_t i = 0; i + 1 < groups.size(); i += 2) {
+      Grp a = groups[i], b = groups[i + 1];
+      Grp m{a.lo, a.len + b.len, new_sub(a.len + b.len, a.lo)};
+      Step st;
+      st.type = Step::SUB_MERGE;
+      st.buf = m.buf;
+      st.src_a = a.buf;
+      st.src_b = b.buf;
+      plan.steps.push_back(st);
+      plan.stats.paper_updates += 1ull << m.len;
+      next.push_back(m);
+    }
+    if (groups.size() & 1) next.push_back(groups.back());
+    groups.swap(next);
+  }
+  plan.stats.n_sub_gates = sub_gates;
+  if (S.src_mode != 1) {
+    // que had a single group: nothing to boost
+    S.src_mode = 2;
+  }
+  return QS_OK;
+}
+
+// ------------------------------------------------------------ make_plan
+int make_plan(const PlanInput& in, const std::vector<IrGate>& gates_in, Plan& plan,
+              std::string& err) {
+  plan = Plan();
+  plan.n = in.n;
+  plan.n_global = in.n_global;
+  plan.nl = in.n - in.n_global;
+  plan.map_in = in.map;
+  plan.stats.n_gates_in = gates_in.size();
+  plan.stats.naive_updates = (uint64_t)gates_in.size() << in.n;
+  Sched S;
+  S.plan = &plan;
+  S.cfg = &in.cfg;
+  std::vector<int> map = in.map;
+  std::vector<IrGate> gates = gates_in;
+  if (in.product_state) {
+    // a basis state is stored at the identity map (qs_set_basis_state)
+    S.basis_phys = in.basis;
+    S.src_mode = 2;
+  }
+  const bool boost = in.product_state && (in.cfg.flags & QS_OPT_BOOST) && in.n >= 2;
+  if (boost) {
+    int rc = booster(S, in.n, gates, err);
+    if (rc) return rc;
+  }
+  const uint64_t before = plan.stats.paper_updates;
+  if (in.cfg.flags & QS_OPT_DIAG)
+    gates = diagonal_detector(gates, in.n, in.cfg.diag_cap, &plan.stats.n_fused_diag);
+  uint64_t full_gates = 0;
+  for (const IrGate& g : gates) full_gates += g.n_src;
+  plan.stats.paper_updates = before + (full_gates << in.n);
+  int rc = schedule(S, 0, in.n, plan.nl, map, std::move(gates), err);
+  if (rc) return rc;
+  if (S.src_mode) flush_source(S);  // circuit left nothing to fuse the source into
+  plan.map_out = map;
+  return QS_OK;
+}
+
+// ------------------------------------------------------------ encoding
+namespace {
+struct Blob {
+  std::vector<unsigned char> b;
+  size_t align(size_t a) {
+    while (b.size() % a) b.push_back(0);
+    return b.size();
+  }
+  template <class T>
+  size_t put(const T* p, size_t n) {
+    size_t off = align(16);
+    const unsigned char* c = reinterpret_cast<const unsigned char*>(p);
+    b.insert(b.end(), c, c + n * sizeof(T));
+    return off;
+  }
+};
+
+int pair_code(int a, int b) {
+  static const int codes[4][4] = {{-1, 0, 1, 2}, {0, -1, 3, 4}, {1, 3, -1, 5}, {2, 4, 5, -1}};
+  return codes[a][b];
+}
+}  // namespace
+
+int encode_pass(const PassPlan& p, int rank, std::vector<unsigned char>& out, std::string& err) {
+  KPass h;
+  memset(&h, 0, sizeof h);
+  h.kernel = p.kernel;
+  h.nl = p.nl;
+  h.rank_base = (u64)rank << p.nl;
+  h.local_mask = (p.nl >= 64) ? ~0ull : ((1ull << p.nl) - 1);
+  h.src_mode = p.src_mode;
+  h.basis = p.basis;
+  std::vector<KOp> kops;
+  std::vector<KGroup> kgroups;
+  std::vector<KShape> kshapes;
+  std::vector<KTerm> kterms;
+  std::vector<double> pool;
+  auto put_mat = [&](const std::vector<cd>& m) {
+    while (pool.size() % 2) pool.push_back(0);
+    int off = (int)pool.size();
+    for (const cd& z : m) {
+      pool.push_back(z.real());
+      pool.push_back(z.imag());
+    }
+    return off;
+  };
+
+  if (p.kernel == KK_SMALL) {
+    h.n_chunks = 1;
+    for (const POp& op : p.ops) {
+      KOp k;
+      memset(&k, 0, sizeof k);
+      if (op.type == POp::DIAG) {
+        k.type = OP_SDIAG;
+        k.data = (int)kterms.size();
+        for (const Mono& m : op.mono) kterms.push_back({m.mask, m.coeff});
+        k.data2 = (int)op.mono.size();
+      } else {
+        k.type = OP_SDENSE;
+        k.k = (uint8_t)op.tpos.size();
+        for (size_t i = 0; i < op.tpos.size(); i++) k.tpos[i] = (int8_t)op.tpos[i];
+        k.ncm = op.cmask;
+        k.data = put_mat(op.mat);
+      }
+      kops.push_back(k);
+    }
+    h.n_ops = (int)kops.size();
+  } else {
+    const int m = (int)p.cpos.size();
+    if (m != kChunkBits) {
+      err = "internal: chunk size";
+      return QS_EINVAL;
+    }
+    for (int c = 0; c < m; c++) {
+      h.cpos[c] = (int8_t)p.cpos[c];
+      h.opos[c] = (int8_t)p.opos[c];
+    }
+    // chunk-id deposit runs over the free local positions
+    u64 cm = 0;
+    for (int c : p.cpos) cm |= 1ull << c;
+    std::vector<int> freep;
+    for (int pos = 0; pos < p.nl; pos++)
+      if (!(cm >> pos & 1)) freep.push_back(pos);
+    h.n_chunks = 1ull << freep.size();
+    int nr = 0;
+    for (size_t i = 0; i < freep.size();) {
+      size_t j = i;
+      while (j + 1 < freep.size() && freep[j + 1] == freep[j] + 1) j++;
+      if (nr >= kMaxRuns) {
+        err = "internal: too many runs";
+        return QS_EINVAL;
+      }
+      h.run_src[nr] = (int8_t)i;
+      h.run_dst[nr] = (int8_t)freep[i];
+      h.run_len[nr] = (int8_t)(j - i + 1);
+      nr++;
+      i = j + 1;
+    }
+    h.n_runs = nr;
+    const int nph = (int)p.phase_regs.size();
+    if (nph > kMaxPhases) {
+      err = "internal: too many phases";
+      return QS_EINVAL;
+    }
+    h.n_phases = nph;
+    // per-phase layouts
+    std::vector<std::vector<int>> thr(nph);
+    for (int ph = 0; ph < nph; ph++) {
+      const std::vector<int>& regs = p.phase_regs[ph];
+      KPhase& kp = h.phases[ph];
+      for (int k = 0; k < kRegBits; k++) kp.reg_c[k] = (int8_t)regs[k];
+      std::vector<int> rest;
+      for (int c = 0; c < m; c++)
+        if (std::find(regs.begin(), regs.end(), c) == regs.end()) rest.push_back(c);
+      // tid bits 0..2: lowest bits of distinct residues mod 3 (bank-conflict
+      // free swizzled exchange), then ascending.
+      std::vector<int> order;
+      for (int res = 0; res < 3; res++)
+        for (int c : rest)
+          if (c % 3 == res && std::find(order.begin(), order.end(), c) == order.end()) {
+            order.push_back(c);
+            break;
+          }
+      std::sort(order.begin(), order.end());
+      for (int c : rest)
+        if (std::find(order.begin(), order.end(), c) == order.end()) order.push_back(c);
+      for (int i = 0; i < kLogT; i++) kp.thr_c[i] = (int8_t)order[i];
+      thr[ph] = order;
+    }
+    auto cbit = [&](int pos) {
+      return (int)(std::find(p.cpos.begin(), p.cpos.end(), pos) - p.cpos.begin());
+    };
+    int cur_phase = -1;
+    for (size_t oi = 0; oi < p.ops.size(); oi++) {
+      const POp& op = p.ops[oi];
+      const int ph = p.op_phase[oi];
+      while (cur_phase < ph) {
+        if (cur_phase >= 0) h.phases[cur_phase].op_end = (int16_t)kops.size();
+        cur_phase++;
+        h.phases[cur_phase].op_begin = (int16_t)kops.size();
+      }
+      const std::vector<int>& regs = p.phase_regs[ph];
+      auto regidx = [&](int c) {
+        return (int)(std::find(regs.begin(), regs.end(), c) - regs.begin());
+      };
+      KOp k;
+      memset(&k, 0, sizeof k);
+      if (op.type == POp::DENSE) {
+        // controls: register bits -> rho mask; the rest stay physical
+        u64 ncm = 0;
+        uint32_t rcm = 0;
+        for (u64 c = op.cmask; c;) {
+          int pos = __builtin_ctzll(c);
+          c &= c - 1;
+          int cb = (pos < p.nl) ? cbit(pos) : m;
+          int ri = (cb < m) ? regidx(cb) : kRegBits;
+          if (ri < kRegBits) rcm |= 1u << ri;
+          else ncm |= 1ull << pos;
+        }
+        k.rcm = rcm;
+        k.ncm = ncm;
+        const int t = (int)op.tpos.size();
+        std::vector<int> rbits(t);
+        for (int i = 0; i < t; i++) {
+          int cb = cbit(op.tpos[i]);
+          rbits[i] = regidx(cb);
+          if (rbits[i] >= kRegBits) {
+            err = "internal: target not in register layout";
+            return QS_EINVAL;
+          }
+        }
+        // permute the matrix so that its bit j <-> j-th smallest register bit
+        std::vector<int> sorted = rbits;
+        std::sort(sorted.begin(), sorted.end());
+        std::vector<int> newbit(t);
+        for (int i = 0; i < t; i++)
+          newbit[i] = (int)(std::find(sorted.begin(), sorted.end(), rbits[i]) - sorted.begin());
+        const int D = 1 << t;
+        std::vector<cd> pm((size_t)D * D);
+        for (int r = 0; r < D; r++)
+          for (int c = 0; c < D; c++) {
+            int r2 = 0, c2 = 0;
+            for (int i = 0; i < t; i++) {
+              r2 |= ((r >> i) & 1) << newbit[i];
+              c2 |= ((c >> i) & 1) << newbit[i];
+            }
+            pm[(size_t)r2 * D + c2] = op.mat[(size_t)r * D + c];
+          }
+        if (t == 1) {
+          k.sel = (uint8_t)rbits[0];
+          if (op.is_h) k.type = OP_H;
+          else if (op.is_x) k.type = OP_X;
+          else { k.type = OP_D1; k.data = put_mat(pm); }
+        } else if (t == 2) {
+          k.type = OP_D2;
+          k.sel = (uint8_t)pair_code(sorted[0], sorted[1]);
+          k.data = put_mat(pm);
+        } else if (t == 3) {
+          k.type = OP_D3;
+          int missing = 0;
+          while (std::find(sorted.begin(), sorted.end(), missing) != sorted.end()) missing++;
+          k.sel = (uint8_t)missing;
+          k.data = put_mat(pm);
+        } else if (t == 4) {
+          k.type = OP_D4;
+          k.data = put_mat(pm);
+        } else {
+          err = "internal: dense op too wide";
+          return QS_EINVAL;
+        }
+      } else {
+        // DIAG: shapes keyed by (register subset R, thread mask)
+        k.type = OP_DIAG;
+        std::map<std::pair<int, uint32_t>, std::vector<KTerm>> shapes;
+        const std::vector<int>& order = thr[ph];
+        for (const Mono& mo : op.mono) {
+          u64 ncmask = 0;
+          int R = 0;
+          uint32_t tm = 0;
+          for (u64 x = mo.mask; x;) {
+            int pos = __builtin_ctzll(x);
+            x &= x - 1;
+            int cb = (pos < p.nl) ? cbit(pos) : m;
+            if (cb >= m) { ncmask |= 1ull << pos; continue; }
+            int ri = regidx(cb);
+            if (ri < kRegBits) { R |= 1 << ri; continue; }
+            int ti = (int)(std::find(order.begin(), order.end(), cb) - order.begin());
+            tm |= 1u << ti;
+          }
+          shapes[{R, tm}].push_back({ncmask, mo.coeff});
+        }
+        KGroup G;
+        memset(&G, 0, sizeof G);
+        int active = 0, has_const = 0;
+        int cnt[kNReg + 1] = {0};
+        for (auto& kv : shapes) cnt[kv.first.first]++;
+        G.rbeg[0] = (int)kshapes.size();
+        for (int R = 0; R < kNReg; R++) G.rbeg[R + 1] = G.rbeg[R] + cnt[R];
+        std::vector<KShape> tmp(shapes.size());
+        int fill[kNReg];
+        for (int R = 0; R < kNReg; R++) fill[R] = G.rbeg[R] - (int)kshapes.size();
+        for (auto& kv : shapes) {
+          const int R = kv.first.first;
+          if (R) active |= R;
+          else has_const = 1;
+          KShape s;
+          memset(&s, 0, sizeof s);
+          s.tmask = kv.first.second;
+          s.term_begin = (int)kterms.size();
+          kterms.insert(kterms.end(), kv.second.begin(), kv.second.end());
+          s.term_end = (int)kterms.size();
+          tmp[fill[R]++] = s;
+        }
+        kshapes.insert(kshapes.end(), tmp.begin(), tmp.end());
+        k.sel = (uint8_t)active;
+        k.has_const = (uint8_t)has_const;
+        k.data = (int)kgroups.size();
+        kgroups.push_back(G);
+      }
+      kops.push_back(k);
+    }
+    while (cur_phase < nph - 1) {
+      if (cur_phase >= 0) h.phases[cur_phase].op_end = (int16_t)kops.size();
+      cur_phase++;
+      h.phases[cur_phase].op_begin = (int16_t)kops.size();
+    }
+    h.phases[nph - 1].op_end = (int16_t)kops.size();
+    h.n_ops = (int)kops.size();
+    h.n_shapes = (int)kshapes.size();
+    h.n_groups = (int)kgroups.size();
+    if (h.n_shapes > kMaxShapes) {
+      err = "internal: too many diagonal shapes in one pass";
+      return QS_EINVAL;
+    }
+  }
+  Blob B;
+  B.put(&h, 1);
+  h.off_ops = (uint32_t)B.put(kops.data(), kops.size());
+  h.off_groups = (uint32_t)B.put(kgroups.data(), kgroups.size());
+  h.off_shapes = (uint32_t)B.put(kshapes.data(), kshapes.size());
+  h.off_terms = (uint32_t)B.put(kterms.data(), kterms.size());
+  h.off_pool = (uint32_t)B.put(pool.data(), pool.size());
+  B.align(16);
+  h.total_bytes = (uint32_t)B.b.size();
+  memcpy(B.b.data(), &h, sizeof h);
+  out.swap(B.b);
+  return QS_OK;
+}
+
+// ------------------------------------------------------------ JSON
+static const char* kname(int k) {
+  switch (k) {
+    case KK_CHUNK: return "K1_chunk";
+    case KK_DENSE: return "K2_dense";
+    case KK_DIAG: return "K3_diag";
+    case KK_SMALL: return "small";
+    default: return "?";
+  }
+}
+
+std::string plan_to_json(const Plan& plan, bool detail) {
+  std::ostringstream o;
+  const PlanStats& s = plan.stats;
+  o << "{\"n\":" << plan.n << ",\"n_global\":" << plan.n_global << ",\"nl\":" << plan.nl;
+  o << ",\"stats\":{\"n_gates_in\":" << s.n_gates_in << ",\"n_passes\":" << s.n_passes
+    << ",\"n_chunk\":" << s.n_chunk << ",\"n_dense\":" << s.n_dense << ",\"n_diag\":" << s.n_diag
+    << ",\"n_small\":" << s.n_small << ",\"n_expand\":" << s.n_expand
+    << ",\"n_swaps\":" << s.n_swaps << ",\"n_sub_gates\":" << s.n_sub_gates
+    << ",\"n_fused_diag\":" << s.n_fused_diag << ",\"paper_updates\":" << s.paper_updates
+    << ",\"naive_updates\":" << s.naive_updates << ",\"bytes_hbm\":" << s.bytes_hbm
+    << ",\"bytes_nvlink\":" << s.bytes_nvlink << ",\"booster_rounds\":[";
+  for (size_t r = 0; r < s.booster_rounds.size(); r++) {
+    o << (r ? "," : "") << "[";
+    for (size_t g = 0; g < s.booster_rounds[r].size(); g++)
+      o << (g ? "," : "") << s.booster_rounds[r][g];
+    o << "]";
+  }
+  o << "]},\"subs\":[";
+  for (size_t i = 0; i < plan.subs.size(); i++)
+    o << (i ? "," : "") << "{\"nq\":" << plan.subs[i].nq << ",\"lo\":" << plan.subs[i].lo << "}";
+  o << "],\"map_in\":[";
+  for (size_t i = 0; i < plan.map_in.size(); i++) o << (i ? "," : "") << plan.map_in[i];
+  o << "],\"map_out\":[";
+  for (size_t i = 0; i < plan.map_out.size(); i++) o << (i ? "," : "") << plan.map_out[i];
+  o << "],\"steps\":[";
+  for (size_t i = 0; i < plan.steps.size(); i++) {
+    const Step& st = plan.steps[i];
+    o << (i ? "," : "") << "{";
+    switch (st.type) {
+      case Step::INIT_BASIS:
+        o << "\"type\":\"init_basis\",\"basis\":\"" << st.basis << "\"";
+        break;
+      case Step::SUB_INIT:
+        o << "\"type\":\"sub_init\",\"buf\":" << st.buf << ",\"basis\":\"" << st.basis << "\"";
+        break;
+      case Step::SUB_MERGE:
+        o << "\"type\":\"sub_merge\",\"buf\":" << st.buf << ",\"a\":" << st.src_a
+          << ",\"b\":" << st.src_b;
+        break;
+      case Step::EXPAND:
+        o << "\"type\":\"expand\",\"bufs\":[";
+        for (size_t k = 0; k < st.exp_bufs.size(); k++) o << (k ? "," : "") << st.exp_bufs[k];
+        o << "],\"exp_lo\":[";
+        for (size_t k = 0; k < st.exp_lo.size(); k++) o << (k ? "," : "") << st.exp_lo[k];
+        o << "],\"exp_len\":[";
+        for (size_t k = 0; k < st.exp_len.size(); k++) o << (k ? "," : "") << st.exp_len[k];
+        o << "]";
+        break;
+      case Step::SWAP:
+      case Step::PERMUTE:
+        o << "\"type\":\"" << (st.type == Step::SWAP ? "swap" : "permute") << "\",\"j\":" << st.j
+          << ",\"gpos\":[";
+        for (size_t k = 0; k < st.gpos.size(); k++) o << (k ? "," : "") << st.gpos[k];
+        o << "],\"lpos\":[";
+        for (size_t k = 0; k < st.lpos.size(); k++) o << (k ? "," : "") << st.lpos[k];
+        o << "]";
+        break;
+      case Step::PASS: {
+        const PassPlan& p = st.pass;
+        o << "\"type\":\"pass\",\"kernel\":\"" << kname(p.kernel) << "\",\"buf\":" << p.buf
+          << ",\"nl\":" << p.nl << ",\"src_mode\":" << p.src_mode
+          << ",\"cpos\":[";
+        for (size_t k = 0; k < p.cpos.size(); k++) o << (k ? "," : "") << p.cpos[k];
+        o << "],\"opos\":[";
+        for (size_t k = 0; k < p.opos.size(); k++) o << (k ? "," : "") << p.opos[k];
+        o << "],\"basis\":\"" << p.basis << "\",\"exp_bufs\":[";
+        for (size_t k = 0; k < p.exp_bufs.size(); k++) o << (k ? "," : "") << p.exp_bufs[k];
+        o << "],\"exp_lo\":[";
+        for (size_t k = 0; k < p.exp_lo.size(); k++) o << (k ? "," : "") << p.exp_lo[k];
+        o << "],\"exp_len\":[";
+        for (size_t k = 0; k < p.exp_len.size(); k++) o << (k ? "," : "") << p.exp_len[k];
+        o << "],\"phase_regs\":[";
+        for (size_t k = 0; k < p.phase_regs.size(); k++) {
+          o << (k ? "," : "") << "[";
+          for (size_t q = 0; q < p.phase_regs[k].size(); q++) o << (q ? "," : "") << p.phase_regs[k][q];
+          o << "]";
+        }
+        o << "],\"phases\":" << p.phase_regs.size() << ",\"ops\":[";
+        for (size_t k = 0; k < p.ops.size(); k++) {
+          const POp& op = p.ops[k];
+          o << (k ? "," : "") << "{\"t\":\"" << (op.type == POp::DIAG ? "diag" : "dense")
+            << "\",\"n_src\":" << op.n_src;
+          if (op.type == POp::DIAG) {
+            o << ",\"n_mono\":" << op.mono.size();
+            if (detail) {
+              o << ",\"mono\":[";
+              for (size_t q = 0; q < op.mono.size(); q++)
+                o << (q ? "," : "") << "[\"" << op.mono[q].mask << "\",\"" << op.mono[q].coeff << "\"]";
+              o << "]";
+            }
+          } else {
+            o << ",\"tpos\":[";
+            for (size_t q = 0; q < op.tpos.size(); q++) o << (q ? "," : "") << op.tpos[q];
+            o << "],\"cmask\":\"" << op.cmask << "\"";
+            if (detail) {
+              char b[64];
+              o << ",\"mat\":[";
+              for (size_t q = 0; q < op.mat.size(); q++) {
+                snprintf(b, sizeof b, "%.17g,%.17g", op.mat[q].real(), op.mat[q].imag());
+                o << (q ? "," : "") << b;
+              }
+              o << "]";
+            }
+          }
+          o << "}";
+        }
+        o << "]";
+        break;
+      }
+    }
+    o << "}";
+  }
+  o << "]}";
+  return o.str();
+}
+
+}  // namespace qs

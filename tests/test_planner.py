@@ -1,0 +1,170 @@
+"""Host optimiser tests (-m "not gpu"): the plan produced by libqs's planner
+(qs_plan_json, no GPU) is replayed by tests/plan_replay.py and compared with
+the CPU oracle, and its structure is checked against the paper's pins
+(Alg. 6 traces, Fig. 2/3 update counts, Fig. 4 grouping)."""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2604_12256_b200 as qs
+import workloads as W
+from tests import pins
+from tests.plan_replay import check_structure, replay
+
+ALL = qs.QS_OPT_ALL
+
+
+def cfg(flags=ALL, fuse=4, diag=0, boost=2):
+    return qs.make_config(flags=flags, fuse_cap=fuse, diag_cap=diag, boost_div=boost)
+
+
+def run(n, gates, ranks=1, c=None, basis=0):
+    plan = qs.plan_json(n, gates, n_ranks=ranks, config=c, product_state=True, basis=basis,
+                        detail=True)
+    check_structure(plan, n, ranks)
+    return plan, replay(plan, n, ranks)
+
+
+# ------------------------------------------------------------------ Alg. 6
+
+def test_divider_traces():
+    # SPEC.md L293-295 / SURVEY App. A
+    assert qs.divider(8, 2) == [2, 2, 2, 2]
+    assert qs.divider(4, 4) == [4]
+    assert qs.divider(5, 2) == [2, 1, 2]
+    assert qs.divider(32, 16) == [16, 16]        # P:L484 two 2^16 sub-states
+    assert qs.divider(30, 8) == [7, 8, 7, 8]
+    assert qs.divider(35, 9) == [8, 9, 9, 9]
+    for n in range(1, 41):
+        for d in range(1, n + 1):
+            assert sum(qs.divider(n, d)) == n
+
+
+# ------------------------------------------------------------------ Fig. 2/3
+
+def test_booster_paper_update_count_f23():
+    """40 * 2^8 = 10,240 naive -> 1,336 with the merge booster
+    (B = 4 -> divSize 2 -> [2,2,2,2]); rounds [[6,6,7,7],[7,4],[3]]."""
+    gates = W.fixture_f23()
+    c = cfg(flags=qs.QS_OPT_BOOST | qs.QS_OPT_BLOCK, boost=4)
+    plan, psi = run(8, gates, c=c)
+    st = plan["stats"]
+    assert st["naive_updates"] == 10240
+    assert st["booster_rounds"] == [[6, 6, 7, 7], [7, 4]]
+    assert st["paper_updates"] == 1336
+    want = oracle.apply_circuit(8, gates)
+    assert np.max(np.abs(psi - want)) < 1e-12
+
+
+# ------------------------------------------------------------------ Fig. 4
+
+def test_detector_fig4_grouping():
+    """RZZ2, RZZ5, CP6, RZZ8, CP9 fuse into one 4-qubit diagonal; H3,
+    RY4 bypassed, RX7 deferred, RZZ11 stopped."""
+    gates = W.fixture_f4()
+    c = cfg(flags=qs.QS_OPT_DIAG | qs.QS_OPT_BLOCK)
+    plan, psi = run(5, gates, c=c)
+    assert plan["stats"]["n_fused_diag"] == 1
+    (p,) = [s for s in plan["steps"] if s["type"] == "pass"]
+    kinds = [(o["t"], o.get("tpos"), o["n_src"]) for o in p["ops"]]
+    # H1, H3, RY4 | D{2,5,6,8,9} | RX7, RY10 | RZZ11
+    assert kinds[0] == ("dense", [0], 1)
+    assert kinds[1] == ("dense", [2], 1)
+    assert kinds[2] == ("dense", [3], 1)
+    assert kinds[3][0] == "diag" and kinds[3][2] == 5
+    assert kinds[4] == ("dense", [0], 1) and kinds[5] == ("dense", [0], 1)
+    assert kinds[6][0] == "diag" and kinds[6][2] == 1
+    want = oracle.apply_circuit(5, gates)
+    assert np.max(np.abs(psi - want)) < 1e-12
+
+
+def test_detector_ablation_random():
+    """with the corrections c4-c7, 0/200 random 4-qubit
+    RZZ/CP/RZ/RX/CX circuits differ from the oracle."""
+    c = cfg(flags=qs.QS_OPT_DIAG | qs.QS_OPT_BLOCK)
+    for seed in range(200):
+        gates = W.random_circuit(4, 14, seed, kinds=["RZZ", "CP", "RZ", "RX", "CX"], max_controls=0)
+        _, psi = run(4, gates, c=c)
+        want = oracle.apply_circuit(4, gates)
+        assert np.max(np.abs(psi - want)) < 1e-12, seed
+
+
+# ------------------------------------------------------------------ replay
+
+FLAGS = [0, qs.QS_OPT_BLOCK, qs.QS_OPT_BLOCK | qs.QS_OPT_FUSE, qs.QS_OPT_DIAG | qs.QS_OPT_BLOCK,
+         qs.QS_OPT_BOOST | qs.QS_OPT_BLOCK, ALL]
+
+
+@pytest.mark.parametrize("flags", FLAGS)
+@pytest.mark.parametrize("seed", range(8))
+def test_replay_random_small(flags, seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(2, 11))
+    gates = W.random_circuit(n, 80, seed, diag_bias=0.4)
+    basis = int(rng.integers(1 << n))
+    _, psi = run(n, gates, c=cfg(flags=flags), basis=basis)
+    want = oracle.apply_circuit(n, gates, x=basis)
+    assert np.max(np.abs(psi - want)) < 1e-11
+
+
+@pytest.mark.parametrize("n,seed", [(13, 0), (14, 1), (15, 2)])
+def test_replay_random_chunked(n, seed):
+    gates = W.random_circuit(n, 150, seed, diag_bias=0.4, max_generic=3)
+    _, psi = run(n, gates, basis=3)
+    want = oracle.apply_circuit(n, gates, x=3)
+    assert np.max(np.abs(psi - want)) < 1e-11
+
+
+@pytest.mark.parametrize("ranks", [2, 4, 8])
+@pytest.mark.parametrize("n", [6, 9, 14])
+def test_replay_sharded(ranks, n):
+    gates = W.random_circuit(n, 120, 10 * n + ranks, diag_bias=0.3)
+    plan, psi = run(n, gates, ranks=ranks, basis=5)
+    want = oracle.apply_circuit(n, gates, x=5)
+    assert np.max(np.abs(psi - want)) < 1e-11
+
+
+@pytest.mark.parametrize("n", [10, 13, 14])
+def test_replay_qft_closed_form(n):
+    for x in (0, 5):
+        plan, psi = run(n, W.qft(n), basis=x)
+        assert np.max(np.abs(psi - pins.qft_closed_form(n, x))) < 1e-12
+
+
+def test_replay_qaoa_sharded():
+    n = 14
+    gates = W.qaoa_maxcut(n, 2, 3)
+    for ranks in (1, 2, 4):
+        plan, psi = run(n, gates, ranks=ranks)
+        want = oracle.apply_circuit(n, gates)
+        assert np.max(np.abs(psi - want)) < 1e-11
+        if ranks > 1:
+            assert plan["stats"]["n_swaps"] >= 1
+
+
+def test_plan_shapes_large():
+    """Plan shape of the benchmark configs (no replay at this size)."""
+    p = qs.plan_json(30, W.qft(30))
+    assert p["stats"]["n_passes"] <= 4
+    p = qs.plan_json(30, W.rzz_full(30))
+    assert p["stats"]["n_passes"] == 1 and p["stats"]["n_diag"] == 1
+    p = qs.plan_json(30, W.diag_chain(30))
+    assert p["stats"]["n_passes"] <= 3
+    p = qs.plan_json(33, W.qft(33), n_ranks=8)
+    assert p["stats"]["n_swaps"] <= 2
+    p = qs.plan_json(35, W.supremacy(5, 7, 20), n_ranks=8)
+    assert p["stats"]["n_passes"] >= 1
+
+
+def test_invalid_gates_rejected():
+    with pytest.raises(qs.QSError):
+        qs.plan_json(3, [W.Gate("H", (3,))])
+    with pytest.raises(qs.QSError):
+        qs.plan_json(3, [W.Gate("CX", (1,), (1,))])
+    bad = np.eye(2) * 1.1
+    with pytest.raises(qs.QSError):
+        qs.plan_json(3, [W.Gate("UNITARY", (0,), (), (), bad)])
+    with pytest.raises(qs.QSError):
+        qs.plan_json(3, [W.Gate("DIAGONAL", (0,), (), (), np.array([1, 2]))])
