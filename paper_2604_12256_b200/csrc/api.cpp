@@ -595,9 +595,12 @@ int qs_create_rank(int n_qubits, int world_size, int rank, int device, const voi
 
 void qs_destroy(qs_ctx* ctx) {
   if (!ctx) return;
-  for (Shard& s : ctx->shards) {
+  for (Shard& s : ctx->shards) {  // loopback shards share one stream: sync all first
     cudaSetDevice(s.device);
     if (s.stream) cudaStreamSynchronize(s.stream);
+  }
+  for (Shard& s : ctx->shards) {
+    cudaSetDevice(s.device);
     if (s.comm) ncclCommDestroy(s.comm);
     cudaFree(s.state);
     cudaFree(s.scratch);

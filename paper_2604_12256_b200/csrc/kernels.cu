@@ -205,6 +205,79 @@ __device__ __forceinline__ void op_diag(double2 (&a)[kNReg], const KOp& op,
   }
 }
 
+// Fast diagonal group: only the empty subset (if has_const) and the linear
+// register bits L have per-thread angles; register-pair terms are constant
+// and pre-multiplied on the host into ck[rho] (16 complex, or null).
+// phase(rho) = E0 * prod_{k in rho & L} E_k * ck[rho]; rho outside `touch`
+// has phase 1 and is skipped.
+template <int L>
+__device__ __forceinline__ void op_phase_fast(double2 (&a)[kNReg], const u64 (&cf)[kRegBits + 1],
+                                              bool has_const, uint32_t touch,
+                                              const double* __restrict__ ck) {
+  double2 E[kRegBits];
+#pragma unroll
+  for (int k = 0; k < kRegBits; k++)
+    if (L >> k & 1) E[k] = cis_turns(cf[1 + k]);
+  const double2 E0 = has_const ? cis_turns(cf[0]) : make_double2(1.0, 0.0);
+#pragma unroll
+  for (int r = 0; r < kNReg; r++) {
+    if (!(touch >> r & 1)) continue;
+    double2 g = E0;
+    bool first = !has_const;
+#pragma unroll
+    for (int k = 0; k < kRegBits; k++)
+      if ((L >> k & 1) && (r >> k & 1)) {
+        g = first ? E[k] : cmul(g, E[k]);
+        first = false;
+      }
+    if (ck) g = first ? ldg2(ck + 2 * r) : cmul(g, ldg2(ck + 2 * r));
+    a[r] = cmul(a[r], g);
+  }
+}
+
+__device__ __forceinline__ void op_diag_fast(double2 (&a)[kNReg], const KOp& op,
+                                             const KGroup* __restrict__ groups,
+                                             const KShape* __restrict__ shapes,
+                                             const double* __restrict__ pool,
+                                             const u64* scoef, uint32_t tid) {
+  const KGroup* G = groups + op.data;
+  u64 cf[kRegBits + 1];
+#pragma unroll
+  for (int i = 0; i <= kRegBits; i++) {
+    const int R = i ? (1 << (i - 1)) : 0;
+    u64 acc = 0;
+    const int e = __ldg(&G->rbeg[R + 1]);
+    for (int j = __ldg(&G->rbeg[R]); j < e; j++) {
+      const uint32_t tm = __ldg(&shapes[j].tmask);
+      if ((tid & tm) == tm) acc += scoef[j];
+    }
+    cf[i] = acc;
+  }
+  const int cko = __ldg(&G->ck_off);
+  const double* ck = (cko >= 0) ? pool + cko : nullptr;
+  const bool hc = op.has_const != 0;
+  const uint32_t touch = op.rcm;
+  switch (op.sel) {
+#define QS_PF(L) case L: op_phase_fast<L>(a, cf, hc, touch, ck); break;
+    QS_PF(0) QS_PF(1) QS_PF(2) QS_PF(3) QS_PF(4) QS_PF(5) QS_PF(6) QS_PF(7)
+    QS_PF(8) QS_PF(9) QS_PF(10) QS_PF(11) QS_PF(12) QS_PF(13) QS_PF(14) QS_PF(15)
+#undef QS_PF
+    default: break;
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void op_hu(double2 (&a)[kNReg]) {
+#pragma unroll
+  for (int r = 0; r < kNReg; r++) {
+    if (r & (1 << K)) continue;
+    const int r1 = r | (1 << K);
+    const double2 x = a[r], y = a[r1];
+    a[r] = make_double2(x.x + y.x, x.y + y.y);
+    a[r1] = make_double2(x.x - y.x, x.y - y.y);
+  }
+}
+
 template <bool DIAG_ONLY>
 __device__ __forceinline__ void apply_ops(double2 (&a)[kNReg], const KOp* __restrict__ ops,
                                           int ob, int oe, const double* __restrict__ pool,
@@ -219,11 +292,24 @@ __device__ __forceinline__ void apply_ops(double2 (&a)[kNReg], const KOp* __rest
     op.rcm = __ldg(&ops[o].rcm);
     op.ncm = __ldg(&ops[o].ncm);
     op.data = __ldg(&ops[o].data);
+    if (op.type == OP_DIAGF) {
+      op_diag_fast(a, op, groups, shapes, pool, scoef, tid);
+      continue;
+    }
     if (op.type == OP_DIAG) {
       op_diag(a, op, groups, shapes, scoef, tid);
       continue;
     }
     if constexpr (!DIAG_ONLY) {
+      if (op.type == OP_HU) {
+        switch (op.sel) {
+          case 0: op_hu<0>(a); break;
+          case 1: op_hu<1>(a); break;
+          case 2: op_hu<2>(a); break;
+          default: op_hu<3>(a); break;
+        }
+        continue;
+      }
       const bool tp = (tphys_full & op.ncm) == op.ncm;
       const double* m = pool + op.data;
       const uint32_t rcm = op.rcm;
@@ -413,6 +499,11 @@ qs_kpass(const unsigned char* __restrict__ blob, double2* __restrict__ state) {
     }
     Layout O;
     make_layout(P, nph - 1, tid, true, O);
+    if (P.scale != 1.0) {
+      const double sc = P.scale;
+#pragma unroll
+      for (int r = 0; r < kNReg; r++) a[r] = make_double2(a[r].x * sc, a[r].y * sc);
+    }
 #pragma unroll
     for (int r = 0; r < kNReg; r++) state[cb | O.tphys | reg_off(O, r)] = a[r];
   }

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <cmath>
 #include <map>
 #include <sstream>
 
@@ -685,6 +686,8 @@ int encode_pass(const PassPlan& p, int rank, std::vector<unsigned char>& out, st
   h.local_mask = (p.nl >= 64) ? ~0ull : ((1ull << p.nl) - 1);
   h.src_mode = p.src_mode;
   h.basis = p.basis;
+  h.scale = 1.0;
+  int n_hu = 0;
   std::vector<KOp> kops;
   std::vector<KGroup> kgroups;
   std::vector<KShape> kshapes;
@@ -843,7 +846,10 @@ int encode_pass(const PassPlan& p, int rank, std::vector<unsigned char>& out, st
           }
         if (t == 1) {
           k.sel = (uint8_t)rbits[0];
-          if (op.is_h) k.type = OP_H;
+          if (op.is_h && rcm == 0 && ncm == 0) {
+            k.type = OP_HU;  // unnormalised; the pass scale restores 1/sqrt2
+            n_hu++;
+          } else if (op.is_h) k.type = OP_H;
           else if (op.is_x) k.type = OP_X;
           else { k.type = OP_D1; k.data = put_mat(pm); }
         } else if (t == 2) {
@@ -886,6 +892,78 @@ int encode_pass(const PassPlan& p, int rank, std::vector<unsigned char>& out, st
         }
         KGroup G;
         memset(&G, 0, sizeof G);
+        G.ck_off = -1;
+        // Fast path (OP_DIAGF) when every shape with >= 2 register bits is
+        // constant (no thread bits, no chunk-dependent terms): those go to a
+        // host table CK16[rho] = exp(2 pi i sum_{R subset rho, |R|>=2} K_R).
+        bool fast = true;
+        for (auto& kv : shapes) {
+          if (popc((u64)kv.first.first) < 2) continue;
+          if (kv.first.second != 0) fast = false;
+          for (const KTerm& tt : kv.second)
+            if (tt.ncmask != 0) fast = false;
+        }
+        if (fast) {
+          u64 K[kNReg] = {0};
+          bool any_pair = false;
+          for (auto it = shapes.begin(); it != shapes.end();) {
+            const int R = it->first.first;
+            if (popc((u64)R) >= 2) {
+              for (const KTerm& tt : it->second) K[R] += tt.coeff;
+              any_pair = true;
+              it = shapes.erase(it);
+            } else {
+              ++it;
+            }
+          }
+          int lin = 0, hc = 0;
+          for (auto& kv : shapes) {
+            if (kv.first.first) lin |= kv.first.first;
+            else hc = 1;
+          }
+          uint32_t touch = 0;
+          std::vector<cd> ck(kNReg, cd(1, 0));
+          for (int r = 0; r < kNReg; r++) {
+            u64 ang = 0;
+            bool nz = false;
+            for (int R = 0; R < kNReg; R++)
+              if (popc((u64)R) >= 2 && (R & ~r) == 0 && K[R]) {
+                ang += K[R];
+                nz = true;
+              }
+            if (nz) {
+              const long double th = (long double)ang / 18446744073709551616.0L * 6.283185307179586476925286766559L;
+              ck[r] = cd((double)cosl(th), (double)sinl(th));
+            }
+            if (hc || (r & lin) || nz) touch |= 1u << r;
+          }
+          if (any_pair) G.ck_off = put_mat(ck);
+          k.type = OP_DIAGF;
+          k.rcm = touch;
+          int cnt[kNReg + 1] = {0};
+          for (auto& kv : shapes) cnt[kv.first.first]++;
+          G.rbeg[0] = (int)kshapes.size();
+          for (int R = 0; R < kNReg; R++) G.rbeg[R + 1] = G.rbeg[R] + cnt[R];
+          int fill[kNReg];
+          std::vector<KShape> tmp(shapes.size());
+          for (int R = 0; R < kNReg; R++) fill[R] = G.rbeg[R] - (int)kshapes.size();
+          for (auto& kv : shapes) {
+            KShape s;
+            memset(&s, 0, sizeof s);
+            s.tmask = kv.first.second;
+            s.term_begin = (int)kterms.size();
+            kterms.insert(kterms.end(), kv.second.begin(), kv.second.end());
+            s.term_end = (int)kterms.size();
+            tmp[fill[kv.first.first]++] = s;
+          }
+          kshapes.insert(kshapes.end(), tmp.begin(), tmp.end());
+          k.sel = (uint8_t)lin;
+          k.has_const = (uint8_t)hc;
+          k.data = (int)kgroups.size();
+          kgroups.push_back(G);
+          kops.push_back(k);
+          continue;
+        }
         int active = 0, has_const = 0;
         int cnt[kNReg + 1] = {0};
         for (auto& kv : shapes) cnt[kv.first.first]++;
@@ -923,6 +1001,8 @@ int encode_pass(const PassPlan& p, int rank, std::vector<unsigned char>& out, st
     h.n_ops = (int)kops.size();
     h.n_shapes = (int)kshapes.size();
     h.n_groups = (int)kgroups.size();
+    // OP_HU leaves a factor sqrt2 per gate: restore 2^{-n_hu/2} at the store
+    h.scale = std::ldexp(1.0, -(n_hu / 2)) * ((n_hu & 1) ? 0.70710678118654752440 : 1.0);
     if (h.n_shapes > kMaxShapes) {
       err = "internal: too many diagonal shapes in one pass";
       return QS_EINVAL;

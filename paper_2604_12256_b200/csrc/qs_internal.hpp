@@ -44,7 +44,11 @@ enum OpType : uint8_t {
   OP_D4 = 4,    // dense 16x16 on all register bits
   OP_H = 5,     // Hadamard on register bit `sel`
   OP_X = 6,     // Pauli X on register bit `sel` (register swap)
-  OP_DIAG = 7,  // phase polynomial group `data`
+  OP_DIAG = 7,  // phase polynomial group `data`, general path (2^a sincos)
+  OP_DIAGF = 8, // fast path: sincos only for the varying empty/linear
+                // register subsets (sel = linear mask L), register-pair
+                // terms constant (host table CK16), rcm = touched-rho mask
+  OP_HU = 9,    // unnormalised Hadamard (x+y, x-y); pass scale at the store
   // SMALL kernel ops (physical positions, whole shard in smem)
   OP_SDENSE = 20,
   OP_SDIAG = 21,
@@ -74,7 +78,7 @@ struct KPhase {
 // subset R, rbeg[R]..rbeg[R+1].
 struct KGroup {
   int32_t rbeg[17];
-  int32_t pad;
+  int32_t ck_off;   // OP_DIAGF: pool offset (doubles) of CK16[16], -1 if none
 };
 
 // A "shape": monomials that agree on their chunk bits.  Its coefficient is
@@ -113,6 +117,8 @@ struct KPass {
   u64 rank_base;       // rank << nl
   u64 local_mask;      // (1 << nl) - 1
   u64 basis;           // src_mode 2: physical index of the 1.0 amplitude
+  double scale;        // multiplies every amplitude at the store (OP_HU)
+  int32_t pad_scale[2];
   int8_t cpos[16];     // physical position of chunk bit c (loads, ops)
   int8_t opos[16];     // physical position of chunk bit c (stores; relabel)
   int8_t run_src[kMaxRuns], run_dst[kMaxRuns], run_len[kMaxRuns];
