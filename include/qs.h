@@ -90,6 +90,10 @@ typedef struct {
   int32_t diag_cap;     /* D: max support of a fused diagonal (0 = no cap)   */
   int32_t boost_div;    /* B: Divider(N, ceil(N/B)) (2)                      */
   uint32_t flags;       /* QS_OPT_* (QS_OPT_ALL)                             */
+  int32_t jit_min_qubits; /* passes over >= this many local qubits run as
+                             per-pass NVRTC-specialised kernels; 0 = all,
+                             > 40 = none.  Default 18 (env QS_JIT=0/1
+                             overrides the default to none / all).          */
 } qs_config_t;
 
 /* ----------------------------------------------------------------- stats */
@@ -226,6 +230,14 @@ int qs_set_timing(qs_ctx *ctx, int enable);
  * caller can record its own CUDA events on the launching stream; NULL if
  * out of range.  Owned by the handle. */
 void *qs_get_stream(const qs_ctx *ctx, int i);
+
+/* Pass specialisation (NVRTC, sm_100a): the chunk/dense/diagonal passes of
+ * large shards are compiled per pass structure and cached (QS_JIT=0|1|auto;
+ * cache directory QS_JIT_CACHE).  Writes a JSON object {jit_launches,
+ * jit_errors, compile_ms, compiles, disk_hits, last_error} (process-wide
+ * compile counters; launch counters of this handle) into buf; returns its
+ * length. */
+int64_t qs_jit_info(const qs_ctx *ctx, char *buf, size_t cap);
 /* launches, summed device ms and ALGORITHMIC bytes (32 B per amplitude per
  * read+write pass, 16 B for write-only passes; swap: bytes sent). */
 int qs_get_kernel_timing(const qs_ctx *ctx, int kernel_id, uint64_t *launches,

@@ -58,7 +58,7 @@ class qs_gate_t(ctypes.Structure):
 class qs_config_t(ctypes.Structure):
     _fields_ = [("chunk_qubits", ctypes.c_int32), ("fuse_cap", ctypes.c_int32),
                 ("diag_cap", ctypes.c_int32), ("boost_div", ctypes.c_int32),
-                ("flags", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("jit_min_qubits", ctypes.c_int32)]
 
 
 class qs_stats_t(ctypes.Structure):
@@ -106,6 +106,7 @@ def load_library(path: str = LIB_PATH):
         "qs_last_launches": (ctypes.c_uint64, [P]),
         "qs_set_timing": (ctypes.c_int, [P, ctypes.c_int]),
         "qs_get_stream": (ctypes.c_void_p, [P, ctypes.c_int]),
+        "qs_jit_info": (ctypes.c_int64, [P, ctypes.c_char_p, ctypes.c_size_t]),
         "qs_get_kernel_timing": (ctypes.c_int, [P, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64),
                                                 ctypes.POINTER(ctypes.c_double),
                                                 ctypes.POINTER(ctypes.c_uint64)]),
@@ -123,8 +124,14 @@ EXPORTED_SYMBOLS = [
     "qs_set_config", "qs_get_config", "qs_default_config", "qs_set_basis_state",
     "qs_apply_circuit", "qs_get_state", "qs_probabilities", "qs_get_stats", "qs_last_error",
     "qs_plan_json", "qs_divider", "qs_last_launches", "qs_set_timing", "qs_get_kernel_timing",
-    "qs_get_stream",
+    "qs_get_stream", "qs_jit_info",
 ]
+
+
+def jit_info(sim=None) -> dict:
+    buf = ctypes.create_string_buffer(1024)
+    load_library().qs_jit_info(sim.h if sim is not None else None, buf, 1024)
+    return json.loads(buf.value.decode())
 
 
 def marshal_gates(gates: Sequence) -> tuple:
@@ -160,8 +167,11 @@ def default_config() -> qs_config_t:
 
 
 def make_config(flags: int = QS_OPT_ALL, fuse_cap: int = 4, diag_cap: int = 0,
-                boost_div: int = 2, chunk_qubits: int = 12) -> qs_config_t:
-    return qs_config_t(chunk_qubits, fuse_cap, diag_cap, boost_div, flags)
+                boost_div: int = 2, chunk_qubits: int = 12,
+                jit_min_qubits: Optional[int] = None) -> qs_config_t:
+    if jit_min_qubits is None:
+        jit_min_qubits = default_config().jit_min_qubits
+    return qs_config_t(chunk_qubits, fuse_cap, diag_cap, boost_div, flags, jit_min_qubits)
 
 
 def plan_json(n_qubits: int, gates: Sequence, n_ranks: int = 1, config: Optional[qs_config_t] = None,

@@ -37,7 +37,35 @@ cudaError_t launch_permute(const double2* in, double2* out, u64 n_amps, const in
                            int n, cudaStream_t st);
 cudaError_t launch_gather(const double2* state, double2* out, u64 off, u64 count, int n,
                           const int8_t* dmap, int nl, u64 rank, int probs, cudaStream_t st);
+bool jit_prepare(const unsigned char* blob, int device, void** fn_out, int* grid_per_sm,
+                 size_t* smem_out, std::string& err, bool compile_only);
+cudaError_t jit_launch(void* fn, int grid, size_t smem, const unsigned char* dblob,
+                       double2* state, u64 rank_base, cudaStream_t st);
+void jit_stats(double* compile_ms, uint64_t* compiles, uint64_t* disk_hits);
+std::string jit_source(const unsigned char* blob);
 }  // namespace qs
+
+namespace {
+// QS_JIT: "0" interpreter kernels only, "1" specialise every chunk/dense/diag
+// pass, unset/"auto": specialise passes over >= 18 local qubits (the tiny
+// sub-state and test passes stay on the interpreter kernels).
+int jit_default_min() {
+  const char* e = getenv("QS_JIT");
+  if (!e || !*e || !strcmp(e, "auto")) return 18;
+  return atoi(e) ? 0 : 99;
+}
+
+int num_sms_of(int device) {
+  static int cache[64] = {0};
+  if (device < 0 || device >= 64) return 148;
+  if (!cache[device]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    cache[device] = v > 0 ? v : 148;
+  }
+  return cache[device];
+}
+}  // namespace
 
 using namespace qs;
 
@@ -91,6 +119,8 @@ struct qs_ctx {
   double* host_tmp = nullptr;           // pinned readout staging
   size_t host_tmp_cap = 0;
   bool timing = true;
+  uint64_t jit_launches = 0, jit_errors = 0;
+  std::string jit_last_error;
   // per kernel kind: launches, ms, algorithmic bytes (last call, shard 0..)
   uint64_t k_count[KK_NUM];
   double k_ms[KK_NUM];
@@ -417,7 +447,21 @@ int execute(qs_ctx* ctx, const Plan& plan) {
           KPass h;
           memcpy(&h, blobs[si].data() + blob_off[si][k], sizeof h);
           double2* buf = (p.buf == 0) ? sh.state : (sh.subpool + sub_off[p.buf]);
-          CU(launch_pass(p.kernel, dblob, h, buf, sh.stream));
+          void* fn = nullptr;
+          int per_sm = 1;
+          size_t smem = 0;
+          std::string jerr;
+          if (p.kernel != KK_SMALL && p.nl >= ctx->cfg.jit_min_qubits &&
+              jit_prepare(blobs[si].data() + blob_off[si][k], sh.device, &fn, &per_sm, &smem, jerr,
+                          false)) {
+            u64 grid = (u64)num_sms_of(sh.device) * per_sm;
+            if (grid > h.n_chunks) grid = h.n_chunks;
+            CU(jit_launch(fn, (int)grid, smem, dblob, buf, h.rank_base, sh.stream));
+            ctx->jit_launches++;
+          } else {
+            if (!jerr.empty()) ctx->jit_errors++, ctx->jit_last_error = jerr;
+            CU(launch_pass(p.kernel, dblob, h, buf, sh.stream));
+          }
           ctx->launches++;
           kind = p.kernel;
           bytes = ((p.src_mode ? 16ull : 32ull) << p.nl);
@@ -484,6 +528,7 @@ void qs_default_config(qs_config_t* cfg) {
   cfg->diag_cap = 0;
   cfg->boost_div = 2;
   cfg->flags = QS_OPT_ALL;
+  cfg->jit_min_qubits = jit_default_min();
 }
 
 static int create_common(qs_ctx* ctx) {
@@ -626,6 +671,7 @@ int qs_set_config(qs_ctx* ctx, const qs_config_t* cfg) {
   if (cfg->diag_cap < 0 || cfg->diag_cap > 64) return set_err(ctx, QS_EINVAL, "diag_cap in [0,64]");
   if (cfg->boost_div < 1 || cfg->boost_div > 64) return set_err(ctx, QS_EINVAL, "boost_div in [1,64]");
   if (cfg->flags & ~QS_OPT_ALL) return set_err(ctx, QS_EINVAL, "unknown flags");
+  if (cfg->jit_min_qubits < 0) return set_err(ctx, QS_EINVAL, "jit_min_qubits >= 0");
   ctx->cfg = *cfg;
   return QS_OK;
 }
@@ -798,6 +844,13 @@ int64_t qs_plan_json(int n_qubits, int n_ranks, const qs_config_t* cfg, int prod
       std::vector<unsigned char> b;
       rc = encode_pass(st.pass, 0, b, err);
       if (rc) return fail(rc);
+      if (detail >= 2 && st.pass.kernel != KK_SMALL) {
+        // compile the specialised kernel (NVRTC works without a GPU)
+        void* fn = nullptr;
+        int per_sm = 0;
+        size_t smem = 0;
+        if (!jit_prepare(b.data(), 0, &fn, &per_sm, &smem, err, true)) return fail(QS_EINVAL);
+      }
     }
   std::string js = plan_to_json(plan, detail != 0);
   if (buf && cap) {
@@ -818,6 +871,29 @@ int qs_divider(int n, int div_size, int* out, int cap) {
 }
 
 uint64_t qs_last_launches(const qs_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int64_t qs_jit_info(const qs_ctx* ctx, char* buf, size_t cap) {
+  double ms = 0;
+  uint64_t nc = 0, hits = 0;
+  jit_stats(&ms, &nc, &hits);
+  char b[512];
+  std::string last = ctx ? ctx->jit_last_error.substr(0, 200) : "";
+  for (char& c : last)
+    if (c == '"' || c == '\\' || c == '\n') c = ' ';
+  snprintf(b, sizeof b,
+           "{\"jit_launches\":%llu,\"jit_errors\":%llu,\"compile_ms\":%.1f,\"compiles\":%llu,"
+           "\"disk_hits\":%llu,\"last_error\":\"%s\"}",
+           (unsigned long long)(ctx ? ctx->jit_launches : 0),
+           (unsigned long long)(ctx ? ctx->jit_errors : 0), ms, (unsigned long long)nc,
+           (unsigned long long)hits, last.c_str());
+  std::string s = b;
+  if (buf && cap) {
+    size_t k = std::min(cap - 1, s.size());
+    memcpy(buf, s.data(), k);
+    buf[k] = 0;
+  }
+  return (int64_t)s.size();
+}
 
 void* qs_get_stream(const qs_ctx* ctx, int i) {
   if (!ctx || i < 0 || i >= (int)ctx->shards.size()) return nullptr;

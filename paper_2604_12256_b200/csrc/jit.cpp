@@ -1,0 +1,627 @@
+// jit.cpp -- per-pass specialisation of the chunk / dense / diagonal kernels
+// (K1/K2/K3) with NVRTC for sm_100a.
+//
+// The planner's pass descriptor (KPass blob) fixes the pass STRUCTURE: chunk
+// positions, register layouts, op sequence, register bits, controls, the
+// diagonal shape masks.  This file turns that structure into straight-line
+// CUDA: every register index, address offset, swizzled shared-memory slot
+// and control test becomes a compile-time constant, X gates become register
+// renames, and the op dispatch of the interpreter kernels (kernels.cu)
+// disappears.  NUMBERS (matrix entries, phase coefficients, constant tables,
+// sub-state pointers, the basis index) are still read from the descriptor at
+// run time, so a circuit with new angles reuses the compiled kernel.
+//
+// Compiled cubins are cached in memory (per device) and on disk
+// (QS_JIT_CACHE, default <libdir>/jit_cache) keyed by a hash of the source.
+// The driver API is reached through cudaGetDriverEntryPoint (no link-time
+// libcuda dependency, so the library still loads on a CPU-only host).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "planner.hpp"
+#include "qs_internal.hpp"
+
+namespace qs {
+
+// ------------------------------------------------------------- source gen
+static const char* kPrelude = R"PRELUDE(
+typedef unsigned long long u64;
+typedef unsigned int u32;
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cmac(double2 acc, double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, fma(-a.y, b.y, acc.x)),
+                      fma(a.x, b.y, fma(a.y, b.x, acc.y)));
+}
+__device__ __forceinline__ double2 cis_turns(u64 t) {
+  const u64 q = (t + (1ull << 61)) >> 62;
+  const long long f = (long long)(t - (q << 62));
+  const double x = (double)f * 3.4061215800865545e-19;
+  const double z = x * x;
+  const double s = fma(x * z,
+      fma(z, fma(z, fma(z, fma(z, fma(z, 1.58969099521155010221e-10,
+      -2.50507602534068634195e-08), 2.75573137070700676789e-06),
+      -1.98412698298579493134e-04), 8.33333333332248946124e-03),
+      -1.66666666666666324348e-01), x);
+  const double c = fma(z * z,
+      fma(z, fma(z, fma(z, fma(z, fma(z, -1.13596475577881948265e-11,
+      2.08757232129817482790e-09), -2.75573143513906633035e-07),
+      2.48015872894767294178e-05), -1.38888888888741095749e-03),
+      4.16666666666666019037e-02), fma(-0.5, z, 1.0));
+  switch ((int)(q & 3)) {
+    case 0: return make_double2(c, s);
+    case 1: return make_double2(-s, c);
+    case 2: return make_double2(-c, -s);
+    default: return make_double2(s, -c);
+  }
+}
+__device__ __forceinline__ int swz(int c) {
+  return c ^ (((c >> 3) ^ (c >> 6) ^ (c >> 9) ^ (c >> 12)) & 7);
+}
+__device__ __forceinline__ double2 ld2(const double* p) {
+  return __ldg(reinterpret_cast<const double2*>(p));
+}
+)PRELUDE";
+
+static int host_swz(int c) { return c ^ (((c >> 3) ^ (c >> 6) ^ (c >> 9) ^ (c >> 12)) & 7); }
+
+static const int kPairA[6] = {0, 0, 0, 1, 1, 2};
+static const int kPairB[6] = {1, 2, 3, 2, 3, 3};
+
+namespace {
+struct Gen {
+  std::ostringstream o;
+  const KPass& h;
+  const KOp* ops;
+  const KGroup* groups;
+  const KShape* shapes;
+  const KTerm* terms;
+  int nm[kNReg];  // register slot -> variable index (X renames)
+  Gen(const KPass& hh, const unsigned char* blob)
+      : h(hh),
+        ops(reinterpret_cast<const KOp*>(blob + hh.off_ops)),
+        groups(reinterpret_cast<const KGroup*>(blob + hh.off_groups)),
+        shapes(reinterpret_cast<const KShape*>(blob + hh.off_shapes)),
+        terms(reinterpret_cast<const KTerm*>(blob + hh.off_terms)) {
+    for (int r = 0; r < kNReg; r++) nm[r] = r;
+  }
+  std::string A(int r) const { return "a" + std::to_string(nm[r]); }
+
+  u64 reg_phys(int p, int r, bool out) const {
+    const int8_t* pos = out ? h.opos : h.cpos;
+    u64 o = 0;
+    for (int k = 0; k < kRegBits; k++)
+      if (r >> k & 1) o |= 1ull << pos[h.phases[p].reg_c[k]];
+    return o;
+  }
+  int reg_slot(int p, int r) const {
+    int c = 0;
+    for (int k = 0; k < kRegBits; k++)
+      if (r >> k & 1) c |= 1 << h.phases[p].reg_c[k];
+    return host_swz(c);
+  }
+  std::string tphys_expr(int p, bool out) const {
+    const int8_t* pos = out ? h.opos : h.cpos;
+    std::string s = "(0ull";
+    for (int i = 0; i < kLogT; i++)
+      s += " | ((u64)((tid >> " + std::to_string(i) + ") & 1u) << " +
+           std::to_string(pos[h.phases[p].thr_c[i]]) + ")";
+    return s + ")";
+  }
+  std::string tc_expr(int p) const {
+    std::string s = "(0";
+    for (int i = 0; i < kLogT; i++)
+      s += " | (int)(((tid >> " + std::to_string(i) + ") & 1u) << " +
+           std::to_string(h.phases[p].thr_c[i]) + ")";
+    return s + ")";
+  }
+  static std::string hex(double d) {
+    char b[64];
+    snprintf(b, sizeof b, "%a", d);
+    return b;
+  }
+  static std::string u(u64 v) { return std::to_string(v) + "ull"; }
+
+  void pred(const KOp& op, int p) {
+    if (op.ncm)
+      o << "    const bool tp = ((cphys | tp" << p << ") & " << u(op.ncm) << ") == " << u(op.ncm)
+        << ";\n    if (tp) {\n";
+    else
+      o << "    {\n";
+  }
+
+  void dense(const KOp& op, int p, int W, const int* bits) {
+    const int D = 1 << W;
+    int tm = 0;
+    for (int b = 0; b < W; b++) tm |= 1 << bits[b];
+    o << "  { // dense " << W << "q\n";
+    pred(op, p);
+    o << "    const double* m = pool + " << op.data << ";\n";
+    if (W <= 2) {
+      for (int i = 0; i < D * D; i++) o << "    const double2 u" << i << " = ld2(m + " << 2 * i << ");\n";
+    }
+    for (int base = 0; base < kNReg; base++) {
+      if (base & tm) continue;
+      if ((base & (int)op.rcm) != (int)op.rcm) continue;
+      int idx[16];
+      for (int i = 0; i < D; i++) {
+        int r = base;
+        for (int b = 0; b < W; b++)
+          if (i >> b & 1) r |= 1 << bits[b];
+        idx[i] = r;
+      }
+      o << "    {\n";
+      for (int i = 0; i < D; i++) o << "      const double2 v" << i << " = " << A(idx[i]) << ";\n";
+      for (int r = 0; r < D; r++) {
+        o << "      " << A(idx[r]) << " = ";
+        std::string acc;
+        for (int c = 0; c < D; c++) {
+          std::string mu = (W <= 2) ? ("u" + std::to_string(r * D + c))
+                                    : ("ld2(m + " + std::to_string(2 * (r * D + c)) + ")");
+          if (c == 0) acc = "cmul(" + mu + ", v0)";
+          else acc = "cmac(" + acc + ", " + mu + ", v" + std::to_string(c) + ")";
+        }
+        o << acc << ";\n";
+      }
+      o << "    }\n";
+    }
+    o << "    }\n  }\n";
+  }
+
+  void hadamard(const KOp& op, int p, bool norm) {
+    const int K = op.sel;
+    o << "  { // H" << (norm ? "" : "u") << "\n";
+    pred(op, p);
+    for (int r = 0; r < kNReg; r++) {
+      if (r >> K & 1) continue;
+      if ((r & (int)op.rcm) != (int)op.rcm) continue;
+      const int r1 = r | (1 << K);
+      o << "      { const double2 x = " << A(r) << ", y = " << A(r1) << ";\n";
+      if (norm) {
+        o << "        " << A(r) << " = make_double2((x.x + y.x) * 0x1.6a09e667f3bcdp-1, (x.y + y.y) * 0x1.6a09e667f3bcdp-1);\n";
+        o << "        " << A(r1) << " = make_double2((x.x - y.x) * 0x1.6a09e667f3bcdp-1, (x.y - y.y) * 0x1.6a09e667f3bcdp-1); }\n";
+      } else {
+        o << "        " << A(r) << " = make_double2(x.x + y.x, x.y + y.y);\n";
+        o << "        " << A(r1) << " = make_double2(x.x - y.x, x.y - y.y); }\n";
+      }
+    }
+    o << "    }\n  }\n";
+  }
+
+  void pauli_x(const KOp& op, int p) {
+    const int K = op.sel;
+    if (op.ncm == 0 && op.rcm == 0) {  // pure register rename: no instructions
+      for (int r = 0; r < kNReg; r++)
+        if (!(r >> K & 1)) std::swap(nm[r], nm[r | (1 << K)]);
+      return;
+    }
+    o << "  { // X (controlled)\n";
+    pred(op, p);
+    for (int r = 0; r < kNReg; r++) {
+      if (r >> K & 1) continue;
+      if ((r & (int)op.rcm) != (int)op.rcm) continue;
+      const int r1 = r | (1 << K);
+      o << "      { const double2 x = " << A(r) << "; " << A(r) << " = " << A(r1) << "; " << A(r1)
+        << " = x; }\n";
+    }
+    o << "    }\n  }\n";
+  }
+
+  // Per-thread sum of the shapes with register subset R.
+  std::string shape_sum(const KGroup& G, int R) const {
+    std::string s = "0ull";
+    for (int j = G.rbeg[R]; j < G.rbeg[R + 1]; j++) {
+      const uint32_t tm = shapes[j].tmask;
+      if (tm == 0) s += " + scoef[" + std::to_string(j) + "]";
+      else
+        s += " + (((tid & " + std::to_string(tm) + "u) == " + std::to_string(tm) + "u) ? scoef[" +
+             std::to_string(j) + "] : 0ull)";
+    }
+    return s;
+  }
+
+  void diag_fast(const KOp& op) {
+    const KGroup& G = groups[op.data];
+    const int L = op.sel;
+    const bool hc = op.has_const != 0;
+    o << "  { // diagonal (fast)\n";
+    if (hc) o << "    const double2 E0 = cis_turns(" << shape_sum(G, 0) << ");\n";
+    for (int k = 0; k < kRegBits; k++)
+      if (L >> k & 1) o << "    const double2 E" << k + 1 << " = cis_turns(" << shape_sum(G, 1 << k) << ");\n";
+    for (int r = 0; r < kNReg; r++) {
+      if (!(op.rcm >> r & 1)) continue;
+      std::vector<std::string> f;
+      if (hc) f.push_back("E0");
+      for (int k = 0; k < kRegBits; k++)
+        if ((L >> k & 1) && (r >> k & 1)) f.push_back("E" + std::to_string(k + 1));
+      if (G.ck_off >= 0) f.push_back("ld2(pool + " + std::to_string(G.ck_off + 2 * r) + ")");
+      if (f.empty()) continue;
+      std::string g = f[0];
+      for (size_t i = 1; i < f.size(); i++) g = "cmul(" + g + ", " + f[i] + ")";
+      o << "    " << A(r) << " = cmul(" << A(r) << ", " << g << ");\n";
+    }
+    o << "  }\n";
+  }
+
+  void diag_general(const KOp& op) {
+    const KGroup& G = groups[op.data];
+    const int act = op.sel;
+    o << "  { // diagonal (general)\n";
+    for (int R = 0; R < kNReg; R++) o << "    u64 g" << R << " = " << shape_sum(G, R) << ";\n";
+    for (int k = 0; k < kRegBits; k++)
+      for (int S = 0; S < kNReg; S++)
+        if (S >> k & 1) o << "    g" << S << " += g" << (S ^ (1 << k)) << ";\n";
+    for (int S = 0; S < kNReg; S++) {
+      if (S & ~act) continue;
+      if (S == 0 && !op.has_const) continue;
+      o << "    { const double2 e = cis_turns(g" << S << ");\n";
+      for (int r = 0; r < kNReg; r++)
+        if ((r & act) == S) o << "      " << A(r) << " = cmul(" << A(r) << ", e);\n";
+      o << "    }\n";
+    }
+    o << "  }\n";
+  }
+
+  void emit_ops(int p, bool diag_only) {
+    const KPhase& ph = h.phases[p];
+    for (int i = ph.op_begin; i < ph.op_end; i++) {
+      const KOp& op = ops[i];
+      switch (op.type) {
+        case OP_DIAGF: diag_fast(op); break;
+        case OP_DIAG: diag_general(op); break;
+        default:
+          if (diag_only) break;
+          if (op.type == OP_HU) hadamard(op, p, false);
+          else if (op.type == OP_H) hadamard(op, p, true);
+          else if (op.type == OP_X) pauli_x(op, p);
+          else if (op.type == OP_D1) { int b[1] = {op.sel}; dense(op, p, 1, b); }
+          else if (op.type == OP_D2) { int b[2] = {kPairA[op.sel], kPairB[op.sel]}; dense(op, p, 2, b); }
+          else if (op.type == OP_D3) {
+            int b[3], n = 0;
+            for (int k = 0; k < kRegBits; k++) if (k != op.sel) b[n++] = k;
+            dense(op, p, 3, b);
+          }
+          break;
+      }
+    }
+  }
+
+  std::string build(const char* kname, bool multi, bool diag_only) {
+    const int nph = multi ? h.n_phases : 1;
+    const int nsh = h.n_shapes;
+    std::vector<int> vary, cons;
+    for (int j = 0; j < nsh; j++) {
+      bool v = false;
+      for (int q = shapes[j].term_begin; q < shapes[j].term_end; q++)
+        if (terms[q].ncmask) v = true;
+      (v ? vary : cons).push_back(j);
+    }
+    o << kPrelude;
+    auto emit_arr = [&](const char* name, const std::vector<int>& v) {
+      o << "__device__ const int " << name << "[" << std::max<size_t>(1, v.size()) << "] = {";
+      for (size_t i = 0; i < v.size(); i++) o << (i ? "," : "") << v[i];
+      if (v.empty()) o << "0";
+      o << "};\n";
+    };
+    emit_arr("vmap", vary);
+    emit_arr("cmap", cons);
+    o << "extern \"C\" __global__ void __launch_bounds__(256, 2)\n" << kname
+      << "(const unsigned char* __restrict__ blob, double2* __restrict__ state, u64 rank_base) {\n";
+    o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
+    o << "  double2* sch = reinterpret_cast<double2*>(smem_raw);\n";
+    o << "  u64* scoef = reinterpret_cast<u64*>(smem_raw + " << (multi ? (16 << kChunkBits) : 0) << ");\n";
+    o << "  (void)sch; (void)scoef;\n";
+    o << "  const double* __restrict__ pool = reinterpret_cast<const double*>(blob + " << h.off_pool << ");\n";
+    o << "  const int* __restrict__ shp = reinterpret_cast<const int*>(blob + " << h.off_shapes << ");\n";
+    o << "  const u64* __restrict__ trm = reinterpret_cast<const u64*>(blob + " << h.off_terms << ");\n";
+    o << "  (void)pool; (void)shp; (void)trm;\n";
+    o << "  const u32 tid = threadIdx.x;\n";
+    for (int p = 0; p < nph; p++) {
+      o << "  const u64 tp" << p << " = " << tphys_expr(p, false) << ";\n";
+      if (multi) o << "  const int st" << p << " = swz(" << tc_expr(p) << ");\n";
+    }
+    o << "  const u64 tpo = " << tphys_expr(nph - 1, true) << ";\n";
+    // level 1, constant shapes: once
+    auto level1 = [&](const char* map, size_t n, bool use_cphys) {
+      o << "    for (int jj = tid; jj < " << n << "; jj += 256) {\n"
+        << "      const int j = " << map << "[jj];\n"
+        << "      const int b = __ldg(shp + 4 * j + 1), e = __ldg(shp + 4 * j + 2);\n"
+        << "      u64 acc = 0ull;\n"
+        << "      for (int q = b; q < e; q++) {\n";
+      if (use_cphys)
+        o << "        const u64 mk = __ldg(trm + 2 * q);\n"
+          << "        if ((cphys & mk) == mk) acc += __ldg(trm + 2 * q + 1);\n";
+      else
+        o << "        acc += __ldg(trm + 2 * q + 1);\n";
+      o << "      }\n      scoef[j] = acc;\n    }\n";
+    };
+    if (!cons.empty()) {
+      o << "  {\n";
+      level1("cmap", cons.size(), false);
+      o << "  }\n  __syncthreads();\n";
+    }
+    o << "  double2 a0, a1, a2, a3, a4, a5, a6, a7, a8, a9, a10, a11, a12, a13, a14, a15;\n";
+    o << "  for (u64 chunk = blockIdx.x; chunk < " << u(h.n_chunks) << "; chunk += gridDim.x) {\n";
+    o << "    const u64 cb = 0ull";
+    for (int i = 0; i < h.n_runs; i++)
+      o << " | (((chunk >> " << (int)h.run_src[i] << ") & " << u((1ull << h.run_len[i]) - 1)
+        << ") << " << (int)h.run_dst[i] << ")";
+    o << ";\n    const u64 cphys = cb | rank_base;\n    (void)cphys;\n";
+    if (!vary.empty()) {
+      o << "    __syncthreads();\n";
+      level1("vmap", vary.size(), true);
+      o << "    __syncthreads();\n";
+    }
+    // loads (phase 0)
+    for (int r = 0; r < kNReg; r++) nm[r] = r;
+    if (h.src_mode == 1) {
+      o << "    {\n";
+      for (int g = 0; g < h.expand.n; g++)
+        o << "      const double2* __restrict__ sv" << g << " = reinterpret_cast<const double2*>(*reinterpret_cast<const u64*>(blob + "
+          << (size_t)((const unsigned char*)&h.expand.ptr[g] - (const unsigned char*)&h) << "));\n";
+      for (int r = 0; r < kNReg; r++) {
+        o << "      { const u64 ph = cphys | tp0 | " << u(reg_phys(0, r, false)) << "; double2 v = ";
+        for (int g = 0; g < h.expand.n; g++) {
+          std::string ld = "__ldg(sv" + std::to_string(g) + " + ((ph >> " + std::to_string(h.expand.lo[g]) +
+                           ") & " + u((1ull << h.expand.len[g]) - 1) + "))";
+          if (g == 0) o << ld;
+          else o << "; v = cmul(v, " << ld << ")";
+        }
+        o << "; " << A(r) << " = v; }\n";
+      }
+      o << "    }\n";
+    } else if (h.src_mode == 2) {
+      o << "    { const u64 bz = *reinterpret_cast<const u64*>(blob + "
+        << (size_t)((const unsigned char*)&h.basis - (const unsigned char*)&h) << ");\n";
+      for (int r = 0; r < kNReg; r++)
+        o << "      " << A(r) << " = make_double2(((cphys | tp0 | " << u(reg_phys(0, r, false))
+          << ") == bz) ? 1.0 : 0.0, 0.0);\n";
+      o << "    }\n";
+    } else {
+      o << "    { const double2* __restrict__ sp = state + (cb | tp0);\n";
+      for (int r = 0; r < kNReg; r++) o << "      " << A(r) << " = sp[" << u(reg_phys(0, r, false)) << "];\n";
+      o << "    }\n";
+    }
+    for (int p = 0; p < nph; p++) {
+      if (p > 0) {
+        o << "    __syncthreads();\n";
+        for (int r = 0; r < kNReg; r++)
+          o << "    sch[st" << p - 1 << " ^ " << reg_slot(p - 1, r) << "] = " << A(r) << ";\n";
+        o << "    __syncthreads();\n";
+        for (int r = 0; r < kNReg; r++)
+          o << "    " << A(r) << " = sch[st" << p << " ^ " << reg_slot(p, r) << "];\n";
+      }
+      emit_ops(p, diag_only);
+    }
+    if (h.scale != 1.0) {
+      for (int r = 0; r < kNReg; r++)
+        o << "    " << A(r) << " = make_double2(" << A(r) << ".x * " << hex(h.scale) << ", " << A(r)
+          << ".y * " << hex(h.scale) << ");\n";
+    }
+    o << "    { double2* __restrict__ so = state + (cb | tpo);\n";
+    for (int r = 0; r < kNReg; r++)
+      o << "      so[" << u(reg_phys(nph - 1, r, true)) << "] = " << A(r) << ";\n";
+    o << "    }\n  }\n}\n";
+    return o.str();
+  }
+};
+
+u64 fnv1a(const std::string& s) {
+  u64 h = 1469598103934665603ull;
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+// ---------------------------------------------------------- driver access
+typedef CUresult (*PFN_ModuleLoadData)(CUmodule*, const void*);
+typedef CUresult (*PFN_ModuleGetFunction)(CUfunction*, CUmodule, const char*);
+typedef CUresult (*PFN_LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned,
+                                     unsigned, unsigned, CUstream, void**, void**);
+typedef CUresult (*PFN_FuncSetAttribute)(CUfunction, CUfunction_attribute, int);
+typedef CUresult (*PFN_OccupancyMax)(int*, CUfunction, int, size_t);
+
+struct Driver {
+  bool ok = false;
+  PFN_ModuleLoadData load = nullptr;
+  PFN_ModuleGetFunction getf = nullptr;
+  PFN_LaunchKernel launch = nullptr;
+  PFN_FuncSetAttribute setattr = nullptr;
+  PFN_OccupancyMax occ = nullptr;
+};
+
+Driver& driver() {
+  static Driver d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    auto get = [](const char* name, void** fn) {
+      cudaDriverEntryPointQueryResult q;
+      return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+             q == cudaDriverEntryPointSuccess && *fn;
+    };
+    d.ok = get("cuModuleLoadData", (void**)&d.load) && get("cuModuleGetFunction", (void**)&d.getf) &&
+           get("cuLaunchKernel", (void**)&d.launch) &&
+           get("cuFuncSetAttribute", (void**)&d.setattr) &&
+           get("cuOccupancyMaxActiveBlocksPerMultiprocessor", (void**)&d.occ);
+  });
+  return d;
+}
+
+struct Compiled {
+  CUfunction f = nullptr;
+  int blocks_per_sm = 1;
+  size_t smem = 0;
+};
+
+std::mutex g_mu;
+std::unordered_map<u64, Compiled> g_cache;  // key: hash ^ device
+double g_compile_ms = 0;
+uint64_t g_compiles = 0, g_disk_hits = 0;
+
+std::string cache_dir() {
+  const char* e = getenv("QS_JIT_CACHE");
+  if (e && *e) return e;
+  Dl_info info;
+  if (dladdr((void*)&fnv1a, &info) && info.dli_fname) {
+    std::string p = info.dli_fname;
+    size_t k = p.rfind('/');
+    if (k != std::string::npos) return p.substr(0, k) + "/jit_cache";
+  }
+  return "/tmp/qs_jit_cache";
+}
+
+bool compile_cubin(const std::string& src, const char* kname, std::vector<char>& cubin,
+                   std::string& err) {
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src.c_str(), "qs_pass.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    err = "nvrtcCreateProgram failed";
+    return false;
+  }
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo",
+                        "--fmad=true", "-default-device"};
+  nvrtcResult rc = nvrtcCompileProgram(prog, 5, opts);
+  if (rc != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string log(n, 0);
+    nvrtcGetProgramLog(prog, &log[0]);
+    err = std::string("NVRTC: ") + nvrtcGetErrorString(rc) + "\n" + log.substr(0, 2000);
+    nvrtcDestroyProgram(&prog);
+    return false;
+  }
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  cubin.resize(n);
+  nvrtcGetCUBIN(prog, cubin.data());
+  nvrtcDestroyProgram(&prog);
+  (void)kname;
+  return true;
+}
+}  // namespace
+
+const char* jit_kernel_name(int kernel) {
+  switch (kernel) {
+    case KK_CHUNK: return "qs_k1_chunk_jit";
+    case KK_DENSE: return "qs_k2_dense_jit";
+    default: return "qs_k3_diag_jit";
+  }
+}
+
+std::string jit_source(const unsigned char* blob) {
+  KPass h;
+  memcpy(&h, blob, sizeof h);
+  Gen g(h, blob);
+  return g.build(jit_kernel_name(h.kernel), h.kernel == KK_CHUNK, h.kernel == KK_DIAG);
+}
+
+// Compile (or fetch) the kernel for this pass on `device` (the current
+// device).  Returns false with `err` on failure.
+bool jit_prepare(const unsigned char* blob, int device, void** fn_out, int* grid_per_sm,
+                 size_t* smem_out, std::string& err, bool compile_only) {
+  KPass h;
+  memcpy(&h, blob, sizeof h);
+  const char* kname = jit_kernel_name(h.kernel);
+  const std::string src = jit_source(blob);
+  const u64 hash = fnv1a(src);
+  const size_t smem = (h.kernel == KK_CHUNK ? ((size_t)16 << kChunkBits) : 0) +
+                      (size_t)h.n_shapes * sizeof(u64);
+  std::lock_guard<std::mutex> lk(g_mu);
+  const u64 key = hash ^ ((u64)(device + 1) * 0x9E3779B97F4A7C15ull);
+  auto it = g_cache.find(key);
+  if (it != g_cache.end() && !compile_only) {
+    *fn_out = (void*)it->second.f;
+    *grid_per_sm = it->second.blocks_per_sm;
+    *smem_out = it->second.smem;
+    return true;
+  }
+  char hx[32];
+  snprintf(hx, sizeof hx, "%016llx", (unsigned long long)hash);
+  const std::string dir = cache_dir();
+  const std::string path = dir + "/" + hx + ".cubin";
+  std::vector<char> cubin;
+  FILE* f = fopen(path.c_str(), "rb");
+  if (f) {
+    fseek(f, 0, SEEK_END);
+    long n = ftell(f);
+    fseek(f, 0, SEEK_SET);
+    cubin.resize(n > 0 ? n : 0);
+    if (n <= 0 || fread(cubin.data(), 1, n, f) != (size_t)n) cubin.clear();
+    fclose(f);
+    if (!cubin.empty()) g_disk_hits++;
+  }
+  if (cubin.empty()) {
+    auto t0 = std::chrono::steady_clock::now();
+    if (!compile_cubin(src, kname, cubin, err)) return false;
+    g_compile_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    g_compiles++;
+    mkdir(dir.c_str(), 0755);
+    std::string tmp = path + ".tmp" + std::to_string(getpid());
+    FILE* w = fopen(tmp.c_str(), "wb");
+    if (w) {
+      fwrite(cubin.data(), 1, cubin.size(), w);
+      fclose(w);
+      rename(tmp.c_str(), path.c_str());
+    }
+  }
+  if (compile_only) return true;
+  Driver& d = driver();
+  if (!d.ok) {
+    err = "CUDA driver entry points unavailable";
+    return false;
+  }
+  CUmodule mod;
+  if (d.load(&mod, cubin.data()) != CUDA_SUCCESS) {
+    err = "cuModuleLoadData failed";
+    return false;
+  }
+  Compiled c;
+  if (d.getf(&c.f, mod, kname) != CUDA_SUCCESS) {
+    err = "cuModuleGetFunction failed";
+    return false;
+  }
+  if (smem > 48 * 1024) d.setattr(c.f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
+  int nb = 1;
+  if (d.occ(&nb, c.f, kThreads, smem) != CUDA_SUCCESS || nb < 1) nb = 1;
+  c.blocks_per_sm = nb;
+  c.smem = smem;
+  g_cache[key] = c;
+  *fn_out = (void*)c.f;
+  *grid_per_sm = nb;
+  *smem_out = smem;
+  return true;
+}
+
+cudaError_t jit_launch(void* fn, int grid, size_t smem, const unsigned char* dblob,
+                       double2* state, u64 rank_base, cudaStream_t st) {
+  Driver& d = driver();
+  void* args[] = {(void*)&dblob, (void*)&state, (void*)&rank_base};
+  CUresult r = d.launch((CUfunction)fn, (unsigned)grid, 1, 1, kThreads, 1, 1, (unsigned)smem,
+                        (CUstream)st, args, nullptr);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorLaunchFailure;
+}
+
+void jit_stats(double* compile_ms, uint64_t* compiles, uint64_t* disk_hits) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  *compile_ms = g_compile_ms;
+  *compiles = g_compiles;
+  *disk_hits = g_disk_hits;
+}
+
+}  // namespace qs

@@ -686,6 +686,13 @@ int encode_pass(const PassPlan& p, int rank, std::vector<unsigned char>& out, st
   h.local_mask = (p.nl >= 64) ? ~0ull : ((1ull << p.nl) - 1);
   h.src_mode = p.src_mode;
   h.basis = p.basis;
+  if (p.src_mode == 1) {  // structure of the expansion; pointers patched by the executor
+    h.expand.n = (int)p.exp_lo.size();
+    for (int g = 0; g < h.expand.n && g < kMaxExpand; g++) {
+      h.expand.lo[g] = p.exp_lo[g];
+      h.expand.len[g] = p.exp_len[g];
+    }
+  }
   h.scale = 1.0;
   int n_hu = 0;
   std::vector<KOp> kops;

@@ -68,6 +68,25 @@ def test_random_chunked(qs, n, seed):
     assert maxdiff(psi, oracle.apply_circuit(n, gates, x=7)) < TOL
 
 
+@pytest.mark.parametrize("jit", [0, 99])
+@pytest.mark.parametrize("n,seed", [(13, 10), (15, 11), (17, 12)])
+def test_specialised_vs_interpreter_kernels(qs, jit, n, seed):
+    """Both kernel paths (NVRTC-specialised per pass: jit_min_qubits=0;
+    interpreter: 99) against the oracle, incl. every op type."""
+    gates = W.random_circuit(n, 220, seed, diag_bias=0.4, max_generic=3)
+    gates += W.qft(n)[:40] + W.supremacy(3, n // 3, 3, seed)
+    psi, _ = sim_run(qs, n, gates, basis=5, jit_min_qubits=jit)
+    assert maxdiff(psi, oracle.apply_circuit(n, gates, x=5)) < TOL
+
+
+@pytest.mark.parametrize("jit", [0, 99])
+def test_specialised_sharded_expand(qs, jit):
+    n = 16
+    gates = W.qaoa_maxcut(n, 2, 4) + W.rzz_full(n, 2, h_layer=False)
+    psi, _ = sim_run(qs, n, gates, ranks=2, jit_min_qubits=jit)
+    assert maxdiff(psi, oracle.apply_circuit(n, gates)) < TOL
+
+
 @pytest.mark.parametrize("flags", [0, 1, 3, 5, 9, 15])
 def test_flag_combinations(qs, flags):
     n = 17
