@@ -79,10 +79,29 @@ def _relabel(arr, cpos, opos):
 
 
 def replay(plan: dict, n: int, n_ranks: int) -> np.ndarray:
+    shards = replay_shards(plan, n, n_ranks)
+    mp = plan["map_out"]
+    L = np.arange(1 << n, dtype=np.int64)
+    phys = np.zeros_like(L)
+    for q in range(n):
+        phys |= ((L >> q) & 1) << mp[q]
+    full = np.concatenate(shards)
+    return full[phys]
+
+
+_SUBS = {}
+
+
+def replay_shards(plan: dict, n: int, n_ranks: int, shards=None, subs=None) -> list:
+    """Run the plan's steps on per-rank shards (physical order); returns the
+    shards.  `subs` (booster sub-states) persists across calls if given."""
     g = int(round(math.log2(n_ranks)))
     nl = n - g
-    shards = [np.zeros(1 << nl, dtype=np.complex128) for _ in range(n_ranks)]
-    subs = {}
+    if shards is None:
+        shards = [np.zeros(1 << nl, dtype=np.complex128) for _ in range(n_ranks)]
+    shards = list(shards)
+    if subs is None:
+        subs = _SUBS
     sub_nq = {i + 1: s["nq"] for i, s in enumerate(plan["subs"])}
     local = np.arange(1 << nl, dtype=np.uint64)
 
@@ -166,13 +185,7 @@ def replay(plan: dict, n: int, n_ranks: int) -> np.ndarray:
                     subs[buf] = arr
         else:
             raise ValueError(ty)
-    mp = plan["map_out"]
-    L = np.arange(1 << n, dtype=np.int64)
-    phys = np.zeros_like(L)
-    for q in range(n):
-        phys |= ((L >> q) & 1) << mp[q]
-    full = np.concatenate(shards)
-    return full[phys]
+    return shards
 
 
 def check_structure(plan: dict, n: int, n_ranks: int):
