@@ -76,6 +76,24 @@ __device__ __forceinline__ int swz(int c) {
 __device__ __forceinline__ double2 ld2(const double* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }
+__device__ __forceinline__ u32 sa(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(u64* b, u32 n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(sa(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(u64* b, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(sa(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(sa(dst)), "l"(src), "r"(bytes), "r"(sa(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* b, u32 parity) {
+  asm volatile("{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}"
+               :: "r"(sa(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 )PRELUDE";
 
 static int host_swz(int c) { return c ^ (((c >> 3) ^ (c >> 6) ^ (c >> 9) ^ (c >> 12)) & 7); }
@@ -320,12 +338,43 @@ struct Gen {
     };
     emit_arr("vmap", vary);
     emit_arr("cmap", cons);
+    // Load passes stream their chunks through two shared-memory stages filled
+    // by cp.async.bulk (the TMA bulk-copy engine) one chunk ahead.
+    const bool pipe = (h.src_mode == 0);
+    const int CH = 1 << kChunkBits;
+    int l = 0;
+    while (l < kChunkBits && h.cpos[l] == l) l++;
+    const int nseg = 1 << (kChunkBits - l);
+    std::string cbexpr = "0ull";
+    for (int i = 0; i < h.n_runs; i++)
+      cbexpr += " | (((chunk >> " + std::to_string((int)h.run_src[i]) + ") & " +
+                u((1ull << h.run_len[i]) - 1) + ") << " + std::to_string((int)h.run_dst[i]) + ")";
+    if (pipe) {
+      o << "__device__ __forceinline__ void issue(const double2* __restrict__ state, u64 chunk, double2* dst, u64* bar, u32 lane) {\n"
+        << "  const u64 cb = " << cbexpr << ";\n"
+        << "  if (lane == 0) mbar_expect(bar, " << CH * 16 << "u);\n"
+        << "  __syncwarp();\n"
+        << "  for (int seg = lane; seg < " << nseg << "; seg += 32) {\n"
+        << "    const u64 off = 0ull";
+      for (int i = 0; i < kChunkBits - l; i++)
+        o << " | ((u64)((seg >> " << i << ") & 1) << " << (int)h.cpos[l + i] << ")";
+      o << ";\n    bulk_g2s(dst + (seg << " << l << "), state + (cb | off), " << (16 << l) << "u, bar);\n"
+        << "  }\n}\n";
+    }
+    // One stage per CTA, two CTAs per SM: the refill of the stage with the
+    // next chunk is issued right after the chunk's last shared-memory read,
+    // so it overlaps the last layout's compute + stores and the other CTA.
     o << "extern \"C\" __global__ void __launch_bounds__(256, 2)\n" << kname
       << "(const unsigned char* __restrict__ blob, double2* __restrict__ state, u64 rank_base) {\n";
-    o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
-    o << "  double2* sch = reinterpret_cast<double2*>(smem_raw);\n";
-    o << "  u64* scoef = reinterpret_cast<u64*>(smem_raw + " << (multi ? (16 << kChunkBits) : 0) << ");\n";
-    o << "  (void)sch; (void)scoef;\n";
+    o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n";
+    const int sch_bytes = (pipe || multi) ? CH * 16 : 0;
+    o << "  double2* stage = reinterpret_cast<double2*>(smem_raw);\n";
+    o << "  double2* sch = stage;\n";
+    o << "  u64* scoef = reinterpret_cast<u64*>(smem_raw + " << sch_bytes << ");\n";
+    o << "  (void)sch; (void)scoef; (void)stage;\n";
+    if (pipe)
+      o << "  u64* mbar = reinterpret_cast<u64*>(smem_raw + " << sch_bytes + ((nsh * 8 + 15) / 16) * 16
+        << ");\n";
     o << "  const double* __restrict__ pool = reinterpret_cast<const double*>(blob + " << h.off_pool << ");\n";
     o << "  const int* __restrict__ shp = reinterpret_cast<const int*>(blob + " << h.off_shapes << ");\n";
     o << "  const u64* __restrict__ trm = reinterpret_cast<const u64*>(blob + " << h.off_terms << ");\n";
@@ -336,6 +385,14 @@ struct Gen {
       if (multi) o << "  const int st" << p << " = swz(" << tc_expr(p) << ");\n";
     }
     o << "  const u64 tpo = " << tphys_expr(nph - 1, true) << ";\n";
+    if (pipe) {
+      o << "  const int tcl0 = " << tc_expr(0) << ";\n";
+      o << "  if (tid == 0) { mbar_init(mbar, 1);\n"
+        << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\"); }\n"
+        << "  __syncthreads();\n"
+        << "  if (tid < 32 && blockIdx.x < " << u(h.n_chunks) << ") issue(state, blockIdx.x, stage, mbar, tid);\n"
+        << "  u32 par = 0;\n";
+    }
     // level 1, constant shapes: once
     auto level1 = [&](const char* map, size_t n, bool use_cphys) {
       o << "    for (int jj = tid; jj < " << n << "; jj += 256) {\n"
@@ -357,11 +414,12 @@ struct Gen {
     }
     o << "  double2 a0, a1, a2, a3, a4, a5, a6, a7, a8, a9, a10, a11, a12, a13, a14, a15;\n";
     o << "  for (u64 chunk = blockIdx.x; chunk < " << u(h.n_chunks) << "; chunk += gridDim.x) {\n";
-    o << "    const u64 cb = 0ull";
-    for (int i = 0; i < h.n_runs; i++)
-      o << " | (((chunk >> " << (int)h.run_src[i] << ") & " << u((1ull << h.run_len[i]) - 1)
-        << ") << " << (int)h.run_dst[i] << ")";
-    o << ";\n    const u64 cphys = cb | rank_base;\n    (void)cphys;\n";
+    const std::string refill =
+        "    __syncthreads();  // every thread is done reading the stage\n"
+        "    if (tid < 32 && chunk + gridDim.x < " + u(h.n_chunks) +
+        ") { fence_proxy_async(); issue(state, chunk + gridDim.x, stage, mbar, tid); }\n";
+    o << "    const u64 cb = " << cbexpr << ";\n";
+    o << "    const u64 cphys = cb | rank_base;\n    (void)cphys;\n";
     if (!vary.empty()) {
       o << "    __syncthreads();\n";
       level1("vmap", vary.size(), true);
@@ -393,9 +451,15 @@ struct Gen {
           << ") == bz) ? 1.0 : 0.0, 0.0);\n";
       o << "    }\n";
     } else {
-      o << "    { const double2* __restrict__ sp = state + (cb | tp0);\n";
-      for (int r = 0; r < kNReg; r++) o << "      " << A(r) << " = sp[" << u(reg_phys(0, r, false)) << "];\n";
-      o << "    }\n";
+      // staged chunk (linear chunk-index layout) -> registers of layout 0
+      o << "    mbar_wait(mbar, par); par ^= 1u;\n";
+      for (int r = 0; r < kNReg; r++) {
+        int rc = 0;
+        for (int k = 0; k < kRegBits; k++)
+          if (r >> k & 1) rc |= 1 << h.phases[0].reg_c[k];
+        o << "    " << A(r) << " = sch[tcl0 | " << rc << "];\n";
+      }
+      if (nph == 1) o << refill;
     }
     for (int p = 0; p < nph; p++) {
       if (p > 0) {
@@ -405,6 +469,7 @@ struct Gen {
         o << "    __syncthreads();\n";
         for (int r = 0; r < kNReg; r++)
           o << "    " << A(r) << " = sch[st" << p << " ^ " << reg_slot(p, r) << "];\n";
+        if (pipe && p == nph - 1) o << refill;
       }
       emit_ops(p, diag_only);
     }
@@ -540,8 +605,10 @@ bool jit_prepare(const unsigned char* blob, int device, void** fn_out, int* grid
   const char* kname = jit_kernel_name(h.kernel);
   const std::string src = jit_source(blob);
   const u64 hash = fnv1a(src);
-  const size_t smem = (h.kernel == KK_CHUNK ? ((size_t)16 << kChunkBits) : 0) +
-                      (size_t)h.n_shapes * sizeof(u64);
+  const bool pipe = (h.src_mode == 0);
+  const size_t chunk_bytes = (size_t)16 << kChunkBits;
+  const size_t smem = ((pipe || h.kernel == KK_CHUNK) ? chunk_bytes : 0) +
+                      (((size_t)h.n_shapes * sizeof(u64) + 15) / 16) * 16 + (pipe ? 16 : 0);
   std::lock_guard<std::mutex> lk(g_mu);
   const u64 key = hash ^ ((u64)(device + 1) * 0x9E3779B97F4A7C15ull);
   auto it = g_cache.find(key);
