@@ -287,6 +287,10 @@ def main():
     e2e = None
     if args.e2e_steps > 0:
         slice_amps = 1 << 20
+        # untimed warm-up of the readout path (NCCL all-reduce setup in rank mode)
+        sim.set_basis_state(x)
+        sim.apply(gates, marshalled=marsh)
+        sim.state(0, slice_amps)
         barrier()
         t0 = time.perf_counter()
         h2d = 0

@@ -109,13 +109,15 @@ struct Gen {
   const KGroup* groups;
   const KShape* shapes;
   const KTerm* terms;
+  const double* pool;  // host copy of the matrix pool (structure detection)
   int nm[kNReg];  // register slot -> variable index (X renames)
   Gen(const KPass& hh, const unsigned char* blob)
       : h(hh),
         ops(reinterpret_cast<const KOp*>(blob + hh.off_ops)),
         groups(reinterpret_cast<const KGroup*>(blob + hh.off_groups)),
         shapes(reinterpret_cast<const KShape*>(blob + hh.off_shapes)),
-        terms(reinterpret_cast<const KTerm*>(blob + hh.off_terms)) {
+        terms(reinterpret_cast<const KTerm*>(blob + hh.off_terms)),
+        pool(reinterpret_cast<const double*>(blob + hh.off_pool)) {
     for (int r = 0; r < kNReg; r++) nm[r] = r;
   }
   std::string A(int r) const { return "a" + std::to_string(nm[r]); }
@@ -170,9 +172,26 @@ struct Gen {
     o << "  { // dense " << W << "q\n";
     pred(op, p);
     o << "    const double* m = pool + " << op.data << ";\n";
-    if (W <= 2) {
-      for (int i = 0; i < D * D; i++) o << "    const double2 u" << i << " = ld2(m + " << 2 * i << ");\n";
+    // Entry structure (zero / real / imaginary / complex) is baked into the
+    // code -- e.g. RX, RY, SX need 4 FP64 per output instead of 8; values stay
+    // run-time data.
+    const double* mv = pool + op.data;
+    std::vector<int> kind(D * D);  // 0 zero, 1 real, 2 imag, 3 complex
+    for (int i = 0; i < D * D; i++) {
+      const double re = mv[2 * i], im = mv[2 * i + 1];
+      kind[i] = (re == 0.0 && im == 0.0) ? 0 : (im == 0.0) ? 1 : (re == 0.0) ? 2 : 3;
+      const std::string e = std::to_string(i);
+      if (W <= 2) {
+        if (kind[i] == 1 || kind[i] == 3) o << "    const double mr" << e << " = m[" << 2 * i << "];\n";
+        if (kind[i] == 2 || kind[i] == 3) o << "    const double mi" << e << " = m[" << 2 * i + 1 << "];\n";
+      }
     }
+    auto mr = [&](int i) {
+      return (W <= 2) ? "mr" + std::to_string(i) : "m[" + std::to_string(2 * i) + "]";
+    };
+    auto mi = [&](int i) {
+      return (W <= 2) ? "mi" + std::to_string(i) : "m[" + std::to_string(2 * i + 1) + "]";
+    };
     for (int base = 0; base < kNReg; base++) {
       if (base & tm) continue;
       if ((base & (int)op.rcm) != (int)op.rcm) continue;
@@ -186,15 +205,36 @@ struct Gen {
       o << "    {\n";
       for (int i = 0; i < D; i++) o << "      const double2 v" << i << " = " << A(idx[i]) << ";\n";
       for (int r = 0; r < D; r++) {
-        o << "      " << A(idx[r]) << " = ";
-        std::string acc;
+        std::string re, im;
+        auto add = [](std::string& acc, const std::string& t, bool neg) {
+          if (acc.empty()) acc = neg ? "-(" + t + ")" : t;
+          else acc += (neg ? " - " : " + ") + t;
+        };
         for (int c = 0; c < D; c++) {
-          std::string mu = (W <= 2) ? ("u" + std::to_string(r * D + c))
-                                    : ("ld2(m + " + std::to_string(2 * (r * D + c)) + ")");
-          if (c == 0) acc = "cmul(" + mu + ", v0)";
-          else acc = "cmac(" + acc + ", " + mu + ", v" + std::to_string(c) + ")";
+          const int i = r * D + c;
+          const std::string v = "v" + std::to_string(c);
+          switch (kind[i]) {
+            case 1:
+              add(re, mr(i) + " * " + v + ".x", false);
+              add(im, mr(i) + " * " + v + ".y", false);
+              break;
+            case 2:
+              add(re, mi(i) + " * " + v + ".y", true);
+              add(im, mi(i) + " * " + v + ".x", false);
+              break;
+            case 3:
+              add(re, mr(i) + " * " + v + ".x", false);
+              add(re, mi(i) + " * " + v + ".y", true);
+              add(im, mr(i) + " * " + v + ".y", false);
+              add(im, mi(i) + " * " + v + ".x", false);
+              break;
+            default:
+              break;
+          }
         }
-        o << acc << ";\n";
+        if (re.empty()) re = "0.0";
+        if (im.empty()) im = "0.0";
+        o << "      " << A(idx[r]) << " = make_double2(" << re << ", " << im << ");\n";
       }
       o << "    }\n";
     }

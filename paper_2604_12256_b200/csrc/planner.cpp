@@ -167,6 +167,18 @@ struct Sched {
 
 static double dense_cost(int k) { return 4.0 * (1 << k); }  // FP64 FMA per amp
 
+// FP64 instructions per output amplitude of a dense matrix as the
+// specialised kernels execute it: 0 per zero entry, 2 per real or purely
+// imaginary entry, 4 per complex entry (averaged over rows).
+static double mat_cost(const std::vector<cd>& m) {
+  size_t D = 1;
+  while (D * D < m.size()) D++;
+  double c = 0;
+  for (const cd& z : m) c += (z == cd(0, 0)) ? 0.0 : (z.imag() == 0.0 || z.real() == 0.0) ? 2.0 : 4.0;
+  return c / (double)D;
+}
+static double op_cost(const std::vector<cd>& m, bool is_h) { return is_h ? 2.0 : mat_cost(m); }
+
 // Emit the pending source as a standalone step (before a swap / small pass).
 static void flush_source(Sched& S) {
   if (S.src_mode == 1) {
@@ -230,13 +242,16 @@ static void fuse_ops(std::vector<POp>& ops, int fuse_cap) {
         if (std::find(uni.begin(), uni.end(), p) == uni.end()) uni.push_back(p);
       std::sort(uni.begin(), uni.end());
       const int ku = (int)uni.size();
-      const double fused = dense_cost(ku);
-      const double parts = (prev.is_h ? 2.0 : dense_cost((int)prev.tpos.size())) +
-                           (op.is_h ? 2.0 : dense_cost((int)op.tpos.size()));
-      if (ku <= std::min(fuse_cap, kRegBits - 1) && fused <= parts) {
+      const double parts = op_cost(prev.mat, prev.is_h) + op_cost(op.mat, op.is_h);
+      if (ku <= std::min(fuse_cap, kRegBits - 1) && dense_cost(ku) / 2 <= parts) {
         std::vector<cd> A = embed(prev.mat, prev.tpos, uni);
         std::vector<cd> B = embed(op.mat, op.tpos, uni);
-        prev.mat = matmul(B, A, 1 << ku);  // later gate applied after
+        std::vector<cd> F = matmul(B, A, 1 << ku);  // later gate applied after
+        if (mat_cost(F) > parts) {
+          out.push_back(std::move(op));
+          continue;
+        }
+        prev.mat = F;
         prev.tpos = uni;
         prev.is_h = prev.is_x = false;
         prev.n_src += op.n_src;
@@ -383,7 +398,7 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
         }
         u64 nn = need | tp;
         if (popc(nn) > kChunkBits) { defer(); continue; }
-        const double c = g.is_h ? 2.0 : dense_cost((int)g.targets.size());
+        const double c = op_cost(g.mat, g.is_h);
         if (cost + c > 200.0 && dense_taken > 0) { stop = true; defer(); continue; }
         if (!blocking && dense_taken > 0) { stop = true; defer(); continue; }
         need = nn;

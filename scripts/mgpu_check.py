@@ -31,9 +31,12 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    obj = [qs.nccl_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(obj, src=0)
-    nid = obj[0]
+
+    def new_id():
+        # every NCCL communicator needs its own unique id
+        obj = [qs.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return obj[0]
     cases = [
         ("random18", 18, W.random_circuit(18, 250, 3, diag_bias=0.3)),
         ("qaoa20", 20, W.qaoa_maxcut(20, 3, 2)),
@@ -45,7 +48,7 @@ def main():
     for name, n, gates in cases:
         for jit in (99, 0):
             cfg = qs.make_config(jit_min_qubits=jit)
-            sim = qs.Simulator(n, rank=rank, world_size=world, device=local, nccl_id=nid, config=cfg)
+            sim = qs.Simulator(n, rank=rank, world_size=world, device=local, nccl_id=new_id(), config=cfg)
             sim.set_basis_state(5)
             sim.apply(gates)
             psi = sim.state()
@@ -61,7 +64,7 @@ def main():
     # large: QFT closed form at 28 + log2(world) qubits, sampled
     n = 28 + int(math.log2(world))
     x = 123456789 % (1 << n)
-    sim = qs.Simulator(n, rank=rank, world_size=world, device=local, nccl_id=nid)
+    sim = qs.Simulator(n, rank=rank, world_size=world, device=local, nccl_id=new_id())
     sim.set_basis_state(x)
     sim.apply(W.qft(n))
     st = sim.stats()
@@ -84,7 +87,7 @@ def main():
     for layer in range(4):
         gates += [W.Gate("RX", (q,), (), (0.1 + 0.01 * q + layer,)) for q in range(n)]
         gates += [W.Gate("CZ", (q + 1,), (q,)) for q in range(n - 1)]
-    sim = qs.Simulator(n, rank=rank, world_size=world, device=local, nccl_id=nid)
+    sim = qs.Simulator(n, rank=rank, world_size=world, device=local, nccl_id=new_id())
     sim.apply(gates)
     psi = sim.state()
     st = sim.stats()
