@@ -355,6 +355,12 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
     std::vector<IrGate> deferred;
     bool stop = false;
     bool progress = false;
+    // FP64-instruction budget per amplitude (reading c15).  A pass whose
+    // source is fused (booster expand / basis: write-only, 16 B/amp) is
+    // given about the FP64 work the HBM time of a write-only pass covers
+    // (~48/amp at 6.5 TB/s and ~18 TFLOP/s FP64), so ALU-heavy work moves to
+    // the following read+write passes; other passes are capacity-limited.
+    const double budget = (buf == 0 && S.src_mode && !small) ? 48.0 : 400.0;
     double cost = 0;
     size_t n_mono = 0;
     int dense_taken = 0;
@@ -376,7 +382,7 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
       if (g.type == IrGate::DIAG) {
         if (s & blocked_nd) { defer(); continue; }
         if (!small && n_mono + g.mono.size() > 4000 && n_mono > 0) { stop = true; defer(); continue; }
-        if (p.ops.empty() || p.ops.back().type != POp::DIAG) cost += 24;
+        if (p.ops.empty() || p.ops.back().type != POp::DIAG) cost += 8;
         add_diag_op(p.ops, g, map);
         n_mono += g.mono.size();
         progress = true;
@@ -398,8 +404,8 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
         }
         u64 nn = need | tp;
         if (popc(nn) > kChunkBits) { defer(); continue; }
-        const double c = op_cost(g.mat, g.is_h);
-        if (cost + c > 200.0 && dense_taken > 0) { stop = true; defer(); continue; }
+        const double c = op_cost(g.mat, g.is_h) + 0.5;
+        if (cost + c > budget && dense_taken > 0) { stop = true; defer(); continue; }
         if (!blocking && dense_taken > 0) { stop = true; defer(); continue; }
         need = nn;
         cost += c;
