@@ -40,7 +40,9 @@ cudaError_t launch_gather(const double2* state, double2* out, u64 off, u64 count
 bool jit_prepare(const unsigned char* blob, int device, void** fn_out, int* grid_per_sm,
                  size_t* smem_out, std::string& err, bool compile_only);
 cudaError_t jit_launch(void* fn, int grid, size_t smem, const unsigned char* dblob,
-                       double2* state, u64 rank_base, cudaStream_t st);
+                       double2* state, u64 rank_base, const void* pool_host, size_t pool_bytes,
+                       cudaStream_t st);
+size_t jit_param_bytes(const unsigned char* blob);
 void jit_stats(double* compile_ms, uint64_t* compiles, uint64_t* disk_hits);
 std::string jit_source(const unsigned char* blob);
 }  // namespace qs
@@ -456,7 +458,10 @@ int execute(qs_ctx* ctx, const Plan& plan) {
                           false)) {
             u64 grid = (u64)num_sms_of(sh.device) * per_sm;
             if (grid > h.n_chunks) grid = h.n_chunks;
-            CU(jit_launch(fn, (int)grid, smem, dblob, buf, h.rank_base, sh.stream));
+            const unsigned char* hb = blobs[si].data() + blob_off[si][k];
+            const size_t pb = jit_param_bytes(hb);
+            CU(jit_launch(fn, (int)grid, smem, dblob, buf, h.rank_base, hb + h.off_pool, pb,
+                          sh.stream));
             ctx->jit_launches++;
           } else {
             if (!jerr.empty()) ctx->jit_errors++, ctx->jit_last_error = jerr;

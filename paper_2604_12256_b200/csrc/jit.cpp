@@ -94,9 +94,18 @@ __device__ __forceinline__ void mbar_wait(u64* b, u32 parity) {
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(sa(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 )PRELUDE";
 
 static int host_swz(int c) { return c ^ (((c >> 3) ^ (c >> 6) ^ (c >> 9) ^ (c >> 12)) & 7); }
+
+// Kernel parameters are limited to 32764 bytes (CUDA 12.1+, sm_70+); the
+// pool is passed by value up to this many doubles (else read from the blob).
+static const size_t kMaxParamPool = 3900;
 
 static const int kPairA[6] = {0, 0, 0, 1, 1, 2};
 static const int kPairB[6] = {1, 2, 3, 2, 3, 3};
@@ -111,6 +120,19 @@ struct Gen {
   const KTerm* terms;
   const double* pool;  // host copy of the matrix pool (structure detection)
   int nm[kNReg];  // register slot -> variable index (X renames)
+  // per-thread factors that multiply every register, not yet applied:
+  // folded into the next full-width diagonal's E0, else applied at the store
+  std::vector<std::string> pend_c;
+  bool pend_scale = false;
+  // pass constants (matrices, CK tables) as a by-value kernel parameter:
+  // FP64 instructions then read them as constant-bank operands
+  bool param_pool = false;
+  std::string pv(int off) const {
+    return (param_pool ? "P.v[" : "pool[") + std::to_string(off) + "]";
+  }
+  // loop-invariant per-thread values hoisted out of the chunk loop
+  std::ostringstream pre;
+  int n_hoist = 0;
   Gen(const KPass& hh, const unsigned char* blob)
       : h(hh),
         ops(reinterpret_cast<const KOp*>(blob + hh.off_ops)),
@@ -171,7 +193,6 @@ struct Gen {
     for (int b = 0; b < W; b++) tm |= 1 << bits[b];
     o << "  { // dense " << W << "q\n";
     pred(op, p);
-    o << "    const double* m = pool + " << op.data << ";\n";
     // Entry structure (zero / real / imaginary / complex) is baked into the
     // code -- e.g. RX, RY, SX need 4 FP64 per output instead of 8; values stay
     // run-time data.
@@ -182,16 +203,12 @@ struct Gen {
       kind[i] = (re == 0.0 && im == 0.0) ? 0 : (im == 0.0) ? 1 : (re == 0.0) ? 2 : 3;
       const std::string e = std::to_string(i);
       if (W <= 2) {
-        if (kind[i] == 1 || kind[i] == 3) o << "    const double mr" << e << " = m[" << 2 * i << "];\n";
-        if (kind[i] == 2 || kind[i] == 3) o << "    const double mi" << e << " = m[" << 2 * i + 1 << "];\n";
+        if (kind[i] == 1 || kind[i] == 3) o << "    const double mr" << e << " = " << pv(op.data + 2 * i) << ";\n";
+        if (kind[i] == 2 || kind[i] == 3) o << "    const double mi" << e << " = " << pv(op.data + 2 * i + 1) << ";\n";
       }
     }
-    auto mr = [&](int i) {
-      return (W <= 2) ? "mr" + std::to_string(i) : "m[" + std::to_string(2 * i) + "]";
-    };
-    auto mi = [&](int i) {
-      return (W <= 2) ? "mi" + std::to_string(i) : "m[" + std::to_string(2 * i + 1) + "]";
-    };
+    auto mr = [&](int i) { return (W <= 2) ? "mr" + std::to_string(i) : pv(op.data + 2 * i); };
+    auto mi = [&](int i) { return (W <= 2) ? "mi" + std::to_string(i) : pv(op.data + 2 * i + 1); };
     for (int base = 0; base < kNReg; base++) {
       if (base & tm) continue;
       if ((base & (int)op.rcm) != (int)op.rcm) continue;
@@ -298,16 +315,42 @@ struct Gen {
     const int L = op.sel;
     const bool hc = op.has_const != 0;
     o << "  { // diagonal (fast)\n";
-    if (hc) o << "    const double2 E0 = cis_turns(" << shape_sum(G, 0) << ");\n";
+    // A slot whose shapes have no chunk-dependent term is loop-invariant per
+    // thread: its sincos is hoisted out of the chunk loop.
+    auto slot_const = [&](int R) {
+      for (int j = G.rbeg[R]; j < G.rbeg[R + 1]; j++)
+        for (int q = shapes[j].term_begin; q < shapes[j].term_end; q++)
+          if (terms[q].ncmask) return false;
+      return true;
+    };
+    auto evar = [&](int R) -> std::string {
+      if (slot_const(R) && n_hoist < 20) {
+        const std::string nmv = "HZ" + std::to_string(n_hoist++);
+        pre << "  const double2 " << nmv << " = cis_turns(" << shape_sum(G, R) << ");\n";
+        return nmv;
+      }
+      return "cis_turns(" + shape_sum(G, R) + ")";
+    };
+    if (hc) {
+      o << "    double2 E0 = " << evar(0) << ";\n";
+      if (op.rcm == 0xFFFFu) {  // multiplies every register: absorb pending factors
+        for (const std::string& f : pend_c) o << "    E0 = cmul(E0, " << f << ");\n";
+        if (pend_scale)
+          o << "    E0 = make_double2(E0.x * " << hex(h.scale) << ", E0.y * " << hex(h.scale) << ");\n";
+        pend_c.clear();
+        pend_scale = false;
+      }
+    }
     for (int k = 0; k < kRegBits; k++)
-      if (L >> k & 1) o << "    const double2 E" << k + 1 << " = cis_turns(" << shape_sum(G, 1 << k) << ");\n";
+      if (L >> k & 1) o << "    const double2 E" << k + 1 << " = " << evar(1 << k) << ";\n";
     for (int r = 0; r < kNReg; r++) {
       if (!(op.rcm >> r & 1)) continue;
       std::vector<std::string> f;
       if (hc) f.push_back("E0");
       for (int k = 0; k < kRegBits; k++)
         if ((L >> k & 1) && (r >> k & 1)) f.push_back("E" + std::to_string(k + 1));
-      if (G.ck_off >= 0) f.push_back("ld2(pool + " + std::to_string(G.ck_off + 2 * r) + ")");
+      if (G.ck_off >= 0)
+        f.push_back("make_double2(" + pv(G.ck_off + 2 * r) + ", " + pv(G.ck_off + 2 * r + 1) + ")");
       if (f.empty()) continue;
       std::string g = f[0];
       for (size_t i = 1; i < f.size(); i++) g = "cmul(" + g + ", " + f[i] + ")";
@@ -389,7 +432,12 @@ struct Gen {
     for (int i = 0; i < h.n_runs; i++)
       cbexpr += " | (((chunk >> " + std::to_string((int)h.run_src[i]) + ") & " +
                 u((1ull << h.run_len[i]) - 1) + ") << " + std::to_string((int)h.run_dst[i]) + ")";
-    if (pipe) {
+    // Refill engine: TMA bulk copies of the chunk's contiguous 2^l-amplitude
+    // runs (l >= 5: >= 512 B each) into a linear stage; for shorter runs
+    // (l = 3, 4: passes that trade coalescing width for target slots) each
+    // thread cp.async's its own 16 layout-0 amplitudes (stage slot r*256+tid).
+    const bool use_tma = pipe && l >= 5;
+    if (use_tma) {
       o << "__device__ __forceinline__ void issue(const double2* __restrict__ state, u64 chunk, double2* dst, u64* bar, u32 lane) {\n"
         << "  const u64 cb = " << cbexpr << ";\n"
         << "  if (lane == 0) mbar_expect(bar, " << CH * 16 << "u);\n"
@@ -400,12 +448,23 @@ struct Gen {
         o << " | ((u64)((seg >> " << i << ") & 1) << " << (int)h.cpos[l + i] << ")";
       o << ";\n    bulk_g2s(dst + (seg << " << l << "), state + (cb | off), " << (16 << l) << "u, bar);\n"
         << "  }\n}\n";
+    } else if (pipe) {
+      o << "__device__ __forceinline__ void issue_async(const double2* __restrict__ state, u64 chunk, double2* stage, u64 tp0, u32 tid) {\n"
+        << "  const u64 cb = " << cbexpr << ";\n"
+        << "  const double2* sp = state + (cb | tp0);\n";
+      for (int r = 0; r < kNReg; r++)
+        o << "  cp_async16(stage + " << r * kThreads << " + tid, sp + " << u(reg_phys(0, r, false)) << ");\n";
+      o << "  cp_async_commit();\n}\n";
     }
     // One stage per CTA, two CTAs per SM: the refill of the stage with the
     // next chunk is issued right after the chunk's last shared-memory read,
     // so it overlaps the last layout's compute + stores and the other CTA.
+    const size_t npool = (h.total_bytes - h.off_pool) / sizeof(double);
+    param_pool = npool > 0 && npool <= kMaxParamPool;
+    if (param_pool) o << "struct QsPool { double v[" << npool << "]; };\n";
     o << "extern \"C\" __global__ void __launch_bounds__(256, 2)\n" << kname
-      << "(const unsigned char* __restrict__ blob, double2* __restrict__ state, u64 rank_base) {\n";
+      << "(const unsigned char* __restrict__ blob, double2* __restrict__ state, u64 rank_base"
+      << (param_pool ? ", const QsPool P" : "") << ") {\n";
     o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n";
     const int sch_bytes = (pipe || multi) ? CH * 16 : 0;
     o << "  double2* stage = reinterpret_cast<double2*>(smem_raw);\n";
@@ -425,13 +484,15 @@ struct Gen {
       if (multi) o << "  const int st" << p << " = swz(" << tc_expr(p) << ");\n";
     }
     o << "  const u64 tpo = " << tphys_expr(nph - 1, true) << ";\n";
-    if (pipe) {
+    if (use_tma) {
       o << "  const int tcl0 = " << tc_expr(0) << ";\n";
       o << "  if (tid == 0) { mbar_init(mbar, 1);\n"
         << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\"); }\n"
         << "  __syncthreads();\n"
         << "  if (tid < 32 && blockIdx.x < " << u(h.n_chunks) << ") issue(state, blockIdx.x, stage, mbar, tid);\n"
         << "  u32 par = 0;\n";
+    } else if (pipe) {
+      o << "  if (blockIdx.x < " << u(h.n_chunks) << ") issue_async(state, blockIdx.x, stage, tp0, tid);\n";
     }
     // level 1, constant shapes: once
     auto level1 = [&](const char* map, size_t n, bool use_cphys) {
@@ -453,11 +514,15 @@ struct Gen {
       o << "  }\n  __syncthreads();\n";
     }
     o << "  double2 a0, a1, a2, a3, a4, a5, a6, a7, a8, a9, a10, a11, a12, a13, a14, a15;\n";
+    const size_t loop_pos = o.str().size();  // hoisted code goes here
     o << "  for (u64 chunk = blockIdx.x; chunk < " << u(h.n_chunks) << "; chunk += gridDim.x) {\n";
     const std::string refill =
-        "    __syncthreads();  // every thread is done reading the stage\n"
-        "    if (tid < 32 && chunk + gridDim.x < " + u(h.n_chunks) +
-        ") { fence_proxy_async(); issue(state, chunk + gridDim.x, stage, mbar, tid); }\n";
+        use_tma ? "    __syncthreads();  // every thread is done reading the stage\n"
+                  "    if (tid < 32 && chunk + gridDim.x < " + u(h.n_chunks) +
+                  ") { fence_proxy_async(); issue(state, chunk + gridDim.x, stage, mbar, tid); }\n"
+                : "    __syncthreads();  // every thread is done reading the stage\n"
+                  "    if (chunk + gridDim.x < " + u(h.n_chunks) +
+                  ") issue_async(state, chunk + gridDim.x, stage, tp0, tid);\n";
     o << "    const u64 cb = " << cbexpr << ";\n";
     o << "    const u64 cphys = cb | rank_base;\n    (void)cphys;\n";
     if (!vary.empty()) {
@@ -467,17 +532,38 @@ struct Gen {
     }
     // loads (phase 0)
     for (int r = 0; r < kNReg; r++) nm[r] = r;
+    pend_c.clear();
+    pend_scale = (h.scale != 1.0);
     if (h.src_mode == 1) {
-      o << "    {\n";
-      for (int g = 0; g < h.expand.n; g++)
-        o << "      const double2* __restrict__ sv" << g << " = reinterpret_cast<const double2*>(*reinterpret_cast<const u64*>(blob + "
+      // groups whose sub-state index ignores the register bits contribute a
+      // per-thread constant factor (loaded once, folded later)
+      u64 regpos = 0;
+      for (int r = 0; r < kNReg; r++) regpos |= reg_phys(0, r, false);
+      std::vector<int> varying;
+      for (int g = 0; g < h.expand.n; g++) {
+        o << "    const double2* __restrict__ sv" << g << " = reinterpret_cast<const double2*>(*reinterpret_cast<const u64*>(blob + "
           << (size_t)((const unsigned char*)&h.expand.ptr[g] - (const unsigned char*)&h) << "));\n";
+        const u64 gmask = ((1ull << h.expand.len[g]) - 1) << h.expand.lo[g];
+        if (regpos & gmask) {
+          varying.push_back(g);
+        } else {
+          o << "    const double2 pf" << g << " = __ldg(sv" << g << " + (((cphys | tp0) >> " << h.expand.lo[g]
+            << ") & " << u((1ull << h.expand.len[g]) - 1) << "));\n";
+          pend_c.push_back("pf" + std::to_string(g));
+        }
+      }
+      o << "    {\n";
       for (int r = 0; r < kNReg; r++) {
+        if (varying.empty()) {
+          o << "      " << A(r) << " = make_double2(1.0, 0.0);\n";
+          continue;
+        }
         o << "      { const u64 ph = cphys | tp0 | " << u(reg_phys(0, r, false)) << "; double2 v = ";
-        for (int g = 0; g < h.expand.n; g++) {
+        for (size_t i = 0; i < varying.size(); i++) {
+          const int g = varying[i];
           std::string ld = "__ldg(sv" + std::to_string(g) + " + ((ph >> " + std::to_string(h.expand.lo[g]) +
                            ") & " + u((1ull << h.expand.len[g]) - 1) + "))";
-          if (g == 0) o << ld;
+          if (i == 0) o << ld;
           else o << "; v = cmul(v, " << ld << ")";
         }
         o << "; " << A(r) << " = v; }\n";
@@ -492,12 +578,17 @@ struct Gen {
       o << "    }\n";
     } else {
       // staged chunk (linear chunk-index layout) -> registers of layout 0
-      o << "    mbar_wait(mbar, par); par ^= 1u;\n";
-      for (int r = 0; r < kNReg; r++) {
-        int rc = 0;
-        for (int k = 0; k < kRegBits; k++)
-          if (r >> k & 1) rc |= 1 << h.phases[0].reg_c[k];
-        o << "    " << A(r) << " = sch[tcl0 | " << rc << "];\n";
+      if (use_tma) {
+        o << "    mbar_wait(mbar, par); par ^= 1u;\n";
+        for (int r = 0; r < kNReg; r++) {
+          int rc = 0;
+          for (int k = 0; k < kRegBits; k++)
+            if (r >> k & 1) rc |= 1 << h.phases[0].reg_c[k];
+          o << "    " << A(r) << " = sch[tcl0 | " << rc << "];\n";
+        }
+      } else {
+        o << "    cp_async_wait_all();  // this thread's own 16 amplitudes\n";
+        for (int r = 0; r < kNReg; r++) o << "    " << A(r) << " = stage[" << r * kThreads << " + tid];\n";
       }
       if (nph == 1) o << refill;
     }
@@ -513,7 +604,13 @@ struct Gen {
       }
       emit_ops(p, diag_only);
     }
-    if (h.scale != 1.0) {
+    if (!pend_c.empty()) {
+      o << "    { double2 F = " << pend_c[0] << ";\n";
+      for (size_t i = 1; i < pend_c.size(); i++) o << "      F = cmul(F, " << pend_c[i] << ");\n";
+      if (pend_scale) o << "      F = make_double2(F.x * " << hex(h.scale) << ", F.y * " << hex(h.scale) << ");\n";
+      for (int r = 0; r < kNReg; r++) o << "      " << A(r) << " = cmul(" << A(r) << ", F);\n";
+      o << "    }\n";
+    } else if (pend_scale) {
       for (int r = 0; r < kNReg; r++)
         o << "    " << A(r) << " = make_double2(" << A(r) << ".x * " << hex(h.scale) << ", " << A(r)
           << ".y * " << hex(h.scale) << ");\n";
@@ -522,7 +619,9 @@ struct Gen {
     for (int r = 0; r < kNReg; r++)
       o << "      so[" << u(reg_phys(nph - 1, r, true)) << "] = " << A(r) << ";\n";
     o << "    }\n  }\n}\n";
-    return o.str();
+    std::string s = o.str();
+    s.insert(loop_pos, pre.str());
+    return s;
   }
 };
 
@@ -715,10 +814,21 @@ bool jit_prepare(const unsigned char* blob, int device, void** fn_out, int* grid
   return true;
 }
 
+// Bytes of the by-value pool parameter of the specialised kernel of this
+// pass (0: the kernel reads its constants from the blob).
+size_t jit_param_bytes(const unsigned char* blob) {
+  KPass h;
+  memcpy(&h, blob, sizeof h);
+  const size_t npool = (h.total_bytes - h.off_pool) / sizeof(double);
+  return (npool > 0 && npool <= kMaxParamPool) ? npool * sizeof(double) : 0;
+}
+
 cudaError_t jit_launch(void* fn, int grid, size_t smem, const unsigned char* dblob,
-                       double2* state, u64 rank_base, cudaStream_t st) {
+                       double2* state, u64 rank_base, const void* pool_host, size_t pool_bytes,
+                       cudaStream_t st) {
   Driver& d = driver();
-  void* args[] = {(void*)&dblob, (void*)&state, (void*)&rank_base};
+  void* args[] = {(void*)&dblob, (void*)&state, (void*)&rank_base, (void*)pool_host};
+  if (!pool_bytes) args[3] = nullptr;
   CUresult r = d.launch((CUfunction)fn, (unsigned)grid, 1, 1, kThreads, 1, 1, (unsigned)smem,
                         (CUstream)st, args, nullptr);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorLaunchFailure;

@@ -335,7 +335,7 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
   Plan& plan = *S.plan;
   const int n_global = nq - nl;
   const bool blocking = (S.cfg->flags & QS_OPT_BLOCK) != 0;
-  const int l = 5;
+  const int l = 3;  // low positions always in a chunk (128 B runs); 3,4 added when room
   std::vector<IrGate> rem = std::move(gates);
   int guard = 0;
   while (!rem.empty()) {
@@ -364,6 +364,8 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
     double cost = 0;
     size_t n_mono = 0;
     int dense_taken = 0;
+    u64 cur_regs = 0;
+    int nphase = 1;
     for (size_t gi = 0; gi < rem.size(); gi++) {
       IrGate& g = rem[gi];
       const u64 s = g.support;
@@ -406,6 +408,20 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
         if (popc(nn) > kChunkBits) { defer(); continue; }
         const double c = op_cost(g.mat, g.is_h) + 0.5;
         if (cost + c > budget && dense_taken > 0) { stop = true; defer(); continue; }
+        // register layouts (assign_phases' greedy, on positions): a new
+        // layout costs a shared-memory exchange; keep <= kMaxPhases/2
+        {
+          const u64 uni = cur_regs | tp;
+          int ph = nphase, cnt = popc(uni);
+          u64 nr = uni;
+          if ((tp & ~cur_regs) && cnt > kRegBits) {
+            ph++;
+            nr = tp;
+          }
+          if (ph > kMaxPhases / 2) { stop = true; defer(); continue; }
+          nphase = ph;
+          cur_regs = nr;
+        }
         if (!blocking && dense_taken > 0) { stop = true; defer(); continue; }
         need = nn;
         cost += c;

@@ -201,7 +201,7 @@ def check_structure(plan: dict, n: int, n_ranks: int):
             continue
         assert pnl > 12
         cpos = st["cpos"]
-        assert len(cpos) == 12 and cpos == sorted(cpos) and set(range(5)) <= set(cpos)
+        assert len(cpos) == 12 and cpos == sorted(cpos) and set(range(3)) <= set(cpos)
         assert 1 <= len(st["phase_regs"]) <= 8
         for op in st["ops"]:
             if op["t"] == "dense":
