@@ -133,6 +133,8 @@ struct Gen {
   // loop-invariant per-thread values hoisted out of the chunk loop
   std::ostringstream pre;
   int n_hoist = 0;
+  int max_hoist = 0;
+  size_t hz_off = 0;  // byte offset of the hoisted-value slots in shared memory
   Gen(const KPass& hh, const unsigned char* blob)
       : h(hh),
         ops(reinterpret_cast<const KOp*>(blob + hh.off_ops)),
@@ -262,14 +264,22 @@ struct Gen {
     const int K = op.sel;
     o << "  { // H" << (norm ? "" : "u") << "\n";
     pred(op, p);
+    // The first unnormalised H of a pass (uncontrolled: touches every
+    // register) also applies the pass's whole 2^{-n/2} scale.
+    std::string f;
+    if (norm) f = "0x1.6a09e667f3bcdp-1";
+    else if (pend_scale && op.rcm == 0 && op.ncm == 0) {
+      f = hex(h.scale);
+      pend_scale = false;
+    }
     for (int r = 0; r < kNReg; r++) {
       if (r >> K & 1) continue;
       if ((r & (int)op.rcm) != (int)op.rcm) continue;
       const int r1 = r | (1 << K);
       o << "      { const double2 x = " << A(r) << ", y = " << A(r1) << ";\n";
-      if (norm) {
-        o << "        " << A(r) << " = make_double2((x.x + y.x) * 0x1.6a09e667f3bcdp-1, (x.y + y.y) * 0x1.6a09e667f3bcdp-1);\n";
-        o << "        " << A(r1) << " = make_double2((x.x - y.x) * 0x1.6a09e667f3bcdp-1, (x.y - y.y) * 0x1.6a09e667f3bcdp-1); }\n";
+      if (!f.empty()) {
+        o << "        " << A(r) << " = make_double2((x.x + y.x) * " << f << ", (x.y + y.y) * " << f << ");\n";
+        o << "        " << A(r1) << " = make_double2((x.x - y.x) * " << f << ", (x.y - y.y) * " << f << "); }\n";
       } else {
         o << "        " << A(r) << " = make_double2(x.x + y.x, x.y + y.y);\n";
         o << "        " << A(r1) << " = make_double2(x.x - y.x, x.y - y.y); }\n";
@@ -323,11 +333,13 @@ struct Gen {
           if (terms[q].ncmask) return false;
       return true;
     };
+    // Hoisted values live in per-thread shared-memory slots (registers are
+    // the scarce resource: keeping them live across the loop spills).
     auto evar = [&](int R) -> std::string {
-      if (slot_const(R) && n_hoist < 20) {
-        const std::string nmv = "HZ" + std::to_string(n_hoist++);
-        pre << "  const double2 " << nmv << " = cis_turns(" << shape_sum(G, R) << ");\n";
-        return nmv;
+      if (slot_const(R) && n_hoist < max_hoist) {
+        const std::string slot = "hz[" + std::to_string(n_hoist++ * kThreads) + " + tid]";
+        pre << "  " << slot << " = cis_turns(" << shape_sum(G, R) << ");\n";
+        return slot;
       }
       return "cis_turns(" + shape_sum(G, R) + ")";
     };
@@ -474,6 +486,11 @@ struct Gen {
     if (pipe)
       o << "  u64* mbar = reinterpret_cast<u64*>(smem_raw + " << sch_bytes + ((nsh * 8 + 15) / 16) * 16
         << ");\n";
+    hz_off = (size_t)sch_bytes + ((nsh * 8 + 15) / 16) * 16 + (pipe ? 16 : 0);
+    // keep 2 CTAs/SM: <= ~110 KB of shared memory per CTA
+    max_hoist = (int)std::max<long>(0, ((long)110 * 1024 - (long)hz_off) / (kThreads * 16));
+    if (max_hoist > 24) max_hoist = 24;
+    o << "  double2* hz = reinterpret_cast<double2*>(smem_raw + " << hz_off << ");\n  (void)hz;\n";
     o << "  const double* __restrict__ pool = reinterpret_cast<const double*>(blob + " << h.off_pool << ");\n";
     o << "  const int* __restrict__ shp = reinterpret_cast<const int*>(blob + " << h.off_shapes << ");\n";
     o << "  const u64* __restrict__ trm = reinterpret_cast<const u64*>(blob + " << h.off_terms << ");\n";
@@ -495,18 +512,21 @@ struct Gen {
       o << "  if (blockIdx.x < " << u(h.n_chunks) << ") issue_async(state, blockIdx.x, stage, tp0, tid);\n";
     }
     // level 1, constant shapes: once
+    // level 1: one warp per shape, lanes over its terms, shuffle reduction
     auto level1 = [&](const char* map, size_t n, bool use_cphys) {
-      o << "    for (int jj = tid; jj < " << n << "; jj += 256) {\n"
+      o << "    for (int jj = (int)(tid >> 5); jj < " << n << "; jj += 8) {\n"
         << "      const int j = " << map << "[jj];\n"
         << "      const int b = __ldg(shp + 4 * j + 1), e = __ldg(shp + 4 * j + 2);\n"
         << "      u64 acc = 0ull;\n"
-        << "      for (int q = b; q < e; q++) {\n";
+        << "      for (int q = b + (int)(tid & 31u); q < e; q += 32) {\n";
       if (use_cphys)
         o << "        const u64 mk = __ldg(trm + 2 * q);\n"
           << "        if ((cphys & mk) == mk) acc += __ldg(trm + 2 * q + 1);\n";
       else
         o << "        acc += __ldg(trm + 2 * q + 1);\n";
-      o << "      }\n      scoef[j] = acc;\n    }\n";
+      o << "      }\n"
+        << "      for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);\n"
+        << "      if ((tid & 31u) == 0) scoef[j] = acc;\n    }\n";
     };
     if (!cons.empty()) {
       o << "  {\n";
@@ -728,11 +748,13 @@ const char* jit_kernel_name(int kernel) {
   }
 }
 
-std::string jit_source(const unsigned char* blob) {
+std::string jit_source(const unsigned char* blob, size_t* smem_bytes = nullptr) {
   KPass h;
   memcpy(&h, blob, sizeof h);
   Gen g(h, blob);
-  return g.build(jit_kernel_name(h.kernel), h.kernel == KK_CHUNK, h.kernel == KK_DIAG);
+  std::string s = g.build(jit_kernel_name(h.kernel), h.kernel == KK_CHUNK, h.kernel == KK_DIAG);
+  if (smem_bytes) *smem_bytes = g.hz_off + (size_t)g.n_hoist * kThreads * 16;
+  return s;
 }
 
 // Compile (or fetch) the kernel for this pass on `device` (the current
@@ -742,12 +764,9 @@ bool jit_prepare(const unsigned char* blob, int device, void** fn_out, int* grid
   KPass h;
   memcpy(&h, blob, sizeof h);
   const char* kname = jit_kernel_name(h.kernel);
-  const std::string src = jit_source(blob);
+  size_t smem = 0;
+  const std::string src = jit_source(blob, &smem);
   const u64 hash = fnv1a(src);
-  const bool pipe = (h.src_mode == 0);
-  const size_t chunk_bytes = (size_t)16 << kChunkBits;
-  const size_t smem = ((pipe || h.kernel == KK_CHUNK) ? chunk_bytes : 0) +
-                      (((size_t)h.n_shapes * sizeof(u64) + 15) / 16) * 16 + (pipe ? 16 : 0);
   std::lock_guard<std::mutex> lk(g_mu);
   const u64 key = hash ^ ((u64)(device + 1) * 0x9E3779B97F4A7C15ull);
   auto it = g_cache.find(key);
