@@ -146,17 +146,31 @@ struct Gen {
   }
   std::string A(int r) const { return "a" + std::to_string(nm[r]); }
 
+  // Register layouts: the pass's phases, plus (when the last one would store
+  // with lanes off the low chunk bits) a store layout reached by one more
+  // shared-memory exchange.
+  std::vector<KPhase> L;
+  static bool lanes_low(const KPhase& k) {  // tid bits 0..2 <-> chunk bits 0..2
+    return k.thr_c[0] == 0 && k.thr_c[1] == 1 && k.thr_c[2] == 2;
+  }
+  static KPhase default_layout() {
+    KPhase k;
+    memset(&k, 0, sizeof k);
+    for (int i = 0; i < kRegBits; i++) k.reg_c[i] = (int8_t)(kChunkBits - kRegBits + i);
+    for (int i = 0; i < kLogT; i++) k.thr_c[i] = (int8_t)i;
+    return k;
+  }
   u64 reg_phys(int p, int r, bool out) const {
     const int8_t* pos = out ? h.opos : h.cpos;
     u64 o = 0;
     for (int k = 0; k < kRegBits; k++)
-      if (r >> k & 1) o |= 1ull << pos[h.phases[p].reg_c[k]];
+      if (r >> k & 1) o |= 1ull << pos[L[p].reg_c[k]];
     return o;
   }
   int reg_slot(int p, int r) const {
     int c = 0;
     for (int k = 0; k < kRegBits; k++)
-      if (r >> k & 1) c |= 1 << h.phases[p].reg_c[k];
+      if (r >> k & 1) c |= 1 << L[p].reg_c[k];
     return host_swz(c);
   }
   std::string tphys_expr(int p, bool out) const {
@@ -164,14 +178,14 @@ struct Gen {
     std::string s = "(0ull";
     for (int i = 0; i < kLogT; i++)
       s += " | ((u64)((tid >> " + std::to_string(i) + ") & 1u) << " +
-           std::to_string(pos[h.phases[p].thr_c[i]]) + ")";
+           std::to_string(pos[L[p].thr_c[i]]) + ")";
     return s + ")";
   }
   std::string tc_expr(int p) const {
     std::string s = "(0";
     for (int i = 0; i < kLogT; i++)
       s += " | (int)(((tid >> " + std::to_string(i) + ") & 1u) << " +
-           std::to_string(h.phases[p].thr_c[i]) + ")";
+           std::to_string(L[p].thr_c[i]) + ")";
     return s + ")";
   }
   static std::string hex(double d) {
@@ -416,6 +430,11 @@ struct Gen {
 
   std::string build(const char* kname, bool multi, bool diag_only) {
     const int nph = multi ? h.n_phases : 1;
+    L.assign(h.phases, h.phases + nph);
+    const bool extra_store = !lanes_low(L[nph - 1]);
+    if (extra_store) L.push_back(default_layout());
+    const int nlay = (int)L.size();
+    const bool xchg = nlay > 1;  // any shared-memory exchange
     const int nsh = h.n_shapes;
     std::vector<int> vary, cons;
     for (int j = 0; j < nsh; j++) {
@@ -448,7 +467,9 @@ struct Gen {
     // runs (l >= 5: >= 512 B each) into a linear stage; for shorter runs
     // (l = 3, 4: passes that trade coalescing width for target slots) each
     // thread cp.async's its own 16 layout-0 amplitudes (stage slot r*256+tid).
-    const bool use_tma = pipe && l >= 5;
+    // the linear TMA stage is conflict-free to read only when layout 0's
+    // lanes sit on the low chunk bits; otherwise per-thread cp.async
+    const bool use_tma = pipe && l >= 5 && lanes_low(L[0]);
     if (use_tma) {
       o << "__device__ __forceinline__ void issue(const double2* __restrict__ state, u64 chunk, double2* dst, u64* bar, u32 lane) {\n"
         << "  const u64 cb = " << cbexpr << ";\n"
@@ -478,7 +499,7 @@ struct Gen {
       << "(const unsigned char* __restrict__ blob, double2* __restrict__ state, u64 rank_base"
       << (param_pool ? ", const QsPool P" : "") << ") {\n";
     o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n";
-    const int sch_bytes = (pipe || multi) ? CH * 16 : 0;
+    const int sch_bytes = (pipe || xchg) ? CH * 16 : 0;
     o << "  double2* stage = reinterpret_cast<double2*>(smem_raw);\n";
     o << "  double2* sch = stage;\n";
     o << "  u64* scoef = reinterpret_cast<u64*>(smem_raw + " << sch_bytes << ");\n";
@@ -496,11 +517,11 @@ struct Gen {
     o << "  const u64* __restrict__ trm = reinterpret_cast<const u64*>(blob + " << h.off_terms << ");\n";
     o << "  (void)pool; (void)shp; (void)trm;\n";
     o << "  const u32 tid = threadIdx.x;\n";
-    for (int p = 0; p < nph; p++) {
+    for (int p = 0; p < nlay; p++) {
       o << "  const u64 tp" << p << " = " << tphys_expr(p, false) << ";\n";
-      if (multi) o << "  const int st" << p << " = swz(" << tc_expr(p) << ");\n";
+      if (xchg) o << "  const int st" << p << " = swz(" << tc_expr(p) << ");\n";
     }
-    o << "  const u64 tpo = " << tphys_expr(nph - 1, true) << ";\n";
+    o << "  const u64 tpo = " << tphys_expr(nlay - 1, true) << ";\n";
     if (use_tma) {
       o << "  const int tcl0 = " << tc_expr(0) << ";\n";
       o << "  if (tid == 0) { mbar_init(mbar, 1);\n"
@@ -603,16 +624,16 @@ struct Gen {
         for (int r = 0; r < kNReg; r++) {
           int rc = 0;
           for (int k = 0; k < kRegBits; k++)
-            if (r >> k & 1) rc |= 1 << h.phases[0].reg_c[k];
+            if (r >> k & 1) rc |= 1 << L[0].reg_c[k];
           o << "    " << A(r) << " = sch[tcl0 | " << rc << "];\n";
         }
       } else {
         o << "    cp_async_wait_all();  // this thread's own 16 amplitudes\n";
         for (int r = 0; r < kNReg; r++) o << "    " << A(r) << " = stage[" << r * kThreads << " + tid];\n";
       }
-      if (nph == 1) o << refill;
+      if (nlay == 1) o << refill;
     }
-    for (int p = 0; p < nph; p++) {
+    for (int p = 0; p < nlay; p++) {
       if (p > 0) {
         o << "    __syncthreads();\n";
         for (int r = 0; r < kNReg; r++)
@@ -620,9 +641,9 @@ struct Gen {
         o << "    __syncthreads();\n";
         for (int r = 0; r < kNReg; r++)
           o << "    " << A(r) << " = sch[st" << p << " ^ " << reg_slot(p, r) << "];\n";
-        if (pipe && p == nph - 1) o << refill;
+        if (pipe && p == nlay - 1) o << refill;
       }
-      emit_ops(p, diag_only);
+      if (p < nph) emit_ops(p, diag_only);
     }
     if (!pend_c.empty()) {
       o << "    { double2 F = " << pend_c[0] << ";\n";
@@ -637,7 +658,7 @@ struct Gen {
     }
     o << "    { double2* __restrict__ so = state + (cb | tpo);\n";
     for (int r = 0; r < kNReg; r++)
-      o << "      so[" << u(reg_phys(nph - 1, r, true)) << "] = " << A(r) << ";\n";
+      o << "      so[" << u(reg_phys(nlay - 1, r, true)) << "] = " << A(r) << ";\n";
     o << "    }\n  }\n}\n";
     std::string s = o.str();
     s.insert(loop_pos, pre.str());

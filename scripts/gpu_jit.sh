@@ -12,3 +12,4 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:qs_k
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/ncu.log
+timeout 600 python scripts/kbench.py > gpurun_out/kbench.log 2>&1
