@@ -150,8 +150,17 @@ struct Gen {
   // with lanes off the low chunk bits) a store layout reached by one more
   // shared-memory exchange.
   std::vector<KPhase> L;
-  static bool lanes_low(const KPhase& k) {  // tid bits 0..2 <-> chunk bits 0..2
-    return k.thr_c[0] == 0 && k.thr_c[1] == 1 && k.thr_c[2] == 2;
+  // number of consecutive low chunk bits (0, 1, ...) held in registers: a
+  // thread then owns 2^run contiguous amplitudes of every register group
+  static int low_run(const KPhase& k) {
+    int run = 0;
+    for (;;) {
+      bool has = false;
+      for (int i = 0; i < kRegBits; i++)
+        if (k.reg_c[i] == run) has = true;
+      if (!has) return run;
+      run++;
+    }
   }
   static KPhase default_layout() {
     KPhase k;
@@ -431,7 +440,9 @@ struct Gen {
   std::string build(const char* kname, bool multi, bool diag_only) {
     const int nph = multi ? h.n_phases : 1;
     L.assign(h.phases, h.phases + nph);
-    const bool extra_store = !lanes_low(L[nph - 1]);
+    // >= 4 contiguous amplitudes per thread at the store: lanes would write
+    // 64+ B apart; one more exchange to the default layout pays for itself
+    const bool extra_store = low_run(L[nph - 1]) >= 2;
     if (extra_store) L.push_back(default_layout());
     const int nlay = (int)L.size();
     const bool xchg = nlay > 1;  // any shared-memory exchange
@@ -467,9 +478,11 @@ struct Gen {
     // runs (l >= 5: >= 512 B each) into a linear stage; for shorter runs
     // (l = 3, 4: passes that trade coalescing width for target slots) each
     // thread cp.async's its own 16 layout-0 amplitudes (stage slot r*256+tid).
-    // the linear TMA stage is conflict-free to read only when layout 0's
-    // lanes sit on the low chunk bits; otherwise per-thread cp.async
-    const bool use_tma = pipe && l >= 5 && lanes_low(L[0]);
+    // The linear TMA stage is read by layout 0 with a 2^run-way bank
+    // conflict; for run >= 2 the chunk is instead copied with coalesced
+    // per-thread cp.async in linear order into XOR-swizzled slots (the
+    // exchange layout), conflict-free on both sides.
+    const bool use_tma = pipe && l >= 5 && low_run(L[0]) <= 1;
     if (use_tma) {
       o << "__device__ __forceinline__ void issue(const double2* __restrict__ state, u64 chunk, double2* dst, u64* bar, u32 lane) {\n"
         << "  const u64 cb = " << cbexpr << ";\n"
@@ -482,11 +495,17 @@ struct Gen {
       o << ";\n    bulk_g2s(dst + (seg << " << l << "), state + (cb | off), " << (16 << l) << "u, bar);\n"
         << "  }\n}\n";
     } else if (pipe) {
-      o << "__device__ __forceinline__ void issue_async(const double2* __restrict__ state, u64 chunk, double2* stage, u64 tp0, u32 tid) {\n"
+      // thread t copies chunk elements c = t + 256 i (coalesced 128 B+ runs)
+      // into slot swz(c) = swz(t) ^ swz(256 i)
+      o << "__device__ __forceinline__ void issue_async(const double2* __restrict__ state, u64 chunk, double2* stage, u64 tpd, int sd) {\n"
         << "  const u64 cb = " << cbexpr << ";\n"
-        << "  const double2* sp = state + (cb | tp0);\n";
-      for (int r = 0; r < kNReg; r++)
-        o << "  cp_async16(stage + " << r * kThreads << " + tid, sp + " << u(reg_phys(0, r, false)) << ");\n";
+        << "  const double2* sp = state + (cb | tpd);\n";
+      for (int i = 0; i < kNReg; i++) {
+        u64 off = 0;
+        for (int k = 0; k < kRegBits; k++)
+          if (i >> k & 1) off |= 1ull << h.cpos[kLogT + k];
+        o << "  cp_async16(stage + (sd ^ " << host_swz(i << kLogT) << "), sp + " << u(off) << ");\n";
+      }
       o << "  cp_async_commit();\n}\n";
     }
     // One stage per CTA, two CTAs per SM: the refill of the stage with the
@@ -519,7 +538,7 @@ struct Gen {
     o << "  const u32 tid = threadIdx.x;\n";
     for (int p = 0; p < nlay; p++) {
       o << "  const u64 tp" << p << " = " << tphys_expr(p, false) << ";\n";
-      if (xchg) o << "  const int st" << p << " = swz(" << tc_expr(p) << ");\n";
+      if (xchg || (pipe && !use_tma)) o << "  const int st" << p << " = swz(" << tc_expr(p) << ");\n";
     }
     o << "  const u64 tpo = " << tphys_expr(nlay - 1, true) << ";\n";
     if (use_tma) {
@@ -530,7 +549,11 @@ struct Gen {
         << "  if (tid < 32 && blockIdx.x < " << u(h.n_chunks) << ") issue(state, blockIdx.x, stage, mbar, tid);\n"
         << "  u32 par = 0;\n";
     } else if (pipe) {
-      o << "  if (blockIdx.x < " << u(h.n_chunks) << ") issue_async(state, blockIdx.x, stage, tp0, tid);\n";
+      std::string tpd = "(0ull";
+      for (int i = 0; i < kLogT; i++)
+        tpd += " | ((u64)((tid >> " + std::to_string(i) + ") & 1u) << " + std::to_string((int)h.cpos[i]) + ")";
+      o << "  const u64 tpd = " << tpd << ");\n  const int sd = swz((int)tid);\n";
+      o << "  if (blockIdx.x < " << u(h.n_chunks) << ") issue_async(state, blockIdx.x, stage, tpd, sd);\n";
     }
     // level 1, constant shapes: once
     // level 1: one warp per shape, lanes over its terms, shuffle reduction
@@ -563,7 +586,7 @@ struct Gen {
                   ") { fence_proxy_async(); issue(state, chunk + gridDim.x, stage, mbar, tid); }\n"
                 : "    __syncthreads();  // every thread is done reading the stage\n"
                   "    if (chunk + gridDim.x < " + u(h.n_chunks) +
-                  ") issue_async(state, chunk + gridDim.x, stage, tp0, tid);\n";
+                  ") issue_async(state, chunk + gridDim.x, stage, tpd, sd);\n";
     o << "    const u64 cb = " << cbexpr << ";\n";
     o << "    const u64 cphys = cb | rank_base;\n    (void)cphys;\n";
     if (!vary.empty()) {
@@ -628,8 +651,8 @@ struct Gen {
           o << "    " << A(r) << " = sch[tcl0 | " << rc << "];\n";
         }
       } else {
-        o << "    cp_async_wait_all();  // this thread's own 16 amplitudes\n";
-        for (int r = 0; r < kNReg; r++) o << "    " << A(r) << " = stage[" << r * kThreads << " + tid];\n";
+        o << "    cp_async_wait_all();\n    __syncthreads();  // every thread's copies have landed\n";
+        for (int r = 0; r < kNReg; r++) o << "    " << A(r) << " = sch[st0 ^ " << reg_slot(0, r) << "];\n";
       }
       if (nlay == 1) o << refill;
     }
