@@ -70,6 +70,19 @@ __device__ __forceinline__ double2 cis_turns(u64 t) {
     default: return make_double2(s, -c);
   }
 }
+// exp(2 pi i t / 2^64) = T[k] * exp(i x): k = nearest 1/256 turn (T in shared
+// memory, filled with cis_turns), |x| <= pi/256; the polynomials' first
+// omitted terms are x^7/7! and x^8/8! (< 1e-17).
+__device__ __forceinline__ double2 cis_tab(u64 t, const double2* __restrict__ T) {
+  const u64 k = (t + (1ull << 55)) >> 56;
+  const long long f = (long long)(t - (k << 56));
+  const double x = (double)f * 3.4061215800865545e-19;
+  const double z = x * x;
+  const double s = x * fma(z, fma(z, 8.3333333333333333e-03, -1.6666666666666667e-01), 1.0);
+  const double c = fma(z, fma(z, fma(z, -1.3888888888888889e-03, 4.1666666666666667e-02), -0.5), 1.0);
+  const double2 b = T[k & 255];
+  return make_double2(fma(b.x, c, -b.y * s), fma(b.x, s, b.y * c));
+}
 __device__ __forceinline__ int swz(int c) {
   return c ^ (((c >> 3) ^ (c >> 6) ^ (c >> 9) ^ (c >> 12)) & 7);
 }
@@ -361,10 +374,10 @@ struct Gen {
     auto evar = [&](int R) -> std::string {
       if (slot_const(R) && n_hoist < max_hoist) {
         const std::string slot = "hz[" + std::to_string(n_hoist++ * kThreads) + " + tid]";
-        pre << "  " << slot << " = cis_turns(" << shape_sum(G, R) << ");\n";
+        pre << "  " << slot << " = cis_tab(" << shape_sum(G, R) << ", ctab);\n";
         return slot;
       }
-      return "cis_turns(" + shape_sum(G, R) + ")";
+      return "cis_tab(" + shape_sum(G, R) + ", ctab)";
     };
     if (hc) {
       o << "    double2 E0 = " << evar(0) << ";\n";
@@ -405,7 +418,7 @@ struct Gen {
     for (int S = 0; S < kNReg; S++) {
       if (S & ~act) continue;
       if (S == 0 && !op.has_const) continue;
-      o << "    { const double2 e = cis_turns(g" << S << ");\n";
+      o << "    { const double2 e = cis_tab(g" << S << ", ctab);\n";
       for (int r = 0; r < kNReg; r++)
         if ((r & act) == S) o << "      " << A(r) << " = cmul(" << A(r) << ", e);\n";
       o << "    }\n";
@@ -461,7 +474,11 @@ struct Gen {
       if (v.empty()) o << "0";
       o << "};\n";
     };
-    emit_arr("vmap", vary);
+    // chunk-dependent shapes: few terms -> one thread each; many -> one warp
+    std::vector<int> vsmall, vbig;
+    for (int j : vary) (shapes[j].term_end - shapes[j].term_begin <= 6 ? vsmall : vbig).push_back(j);
+    emit_arr("vmap", vbig);
+    emit_arr("smap", vsmall);
     emit_arr("cmap", cons);
     // Load passes stream their chunks through two shared-memory stages filled
     // by cp.async.bulk (the TMA bulk-copy engine) one chunk ahead.
@@ -536,6 +553,9 @@ struct Gen {
     o << "  const u64* __restrict__ trm = reinterpret_cast<const u64*>(blob + " << h.off_terms << ");\n";
     o << "  (void)pool; (void)shp; (void)trm;\n";
     o << "  const u32 tid = threadIdx.x;\n";
+    o << "  __shared__ double2 ctab[256];\n"
+      << "  for (int i = (int)tid; i < 256; i += " << kThreads << ") ctab[i] = cis_turns((u64)i << 56);\n"
+      << "  __syncthreads();\n";
     for (int p = 0; p < nlay; p++) {
       o << "  const u64 tp" << p << " = " << tphys_expr(p, false) << ";\n";
       if (xchg || (pipe && !use_tma)) o << "  const int st" << p << " = swz(" << tc_expr(p) << ");\n";
@@ -591,7 +611,16 @@ struct Gen {
     o << "    const u64 cphys = cb | rank_base;\n    (void)cphys;\n";
     if (!vary.empty()) {
       o << "    __syncthreads();\n";
-      level1("vmap", vary.size(), true);
+      if (!vbig.empty()) level1("vmap", vbig.size(), true);
+      if (!vsmall.empty())
+        o << "    for (int jj = (int)tid; jj < " << vsmall.size() << "; jj += " << kThreads << ") {\n"
+          << "      const int j = smap[jj];\n"
+          << "      const int b = __ldg(shp + 4 * j + 1), e = __ldg(shp + 4 * j + 2);\n"
+          << "      u64 acc = 0ull;\n"
+          << "      for (int q = b; q < e; q++) {\n"
+          << "        const u64 mk = __ldg(trm + 2 * q);\n"
+          << "        if ((cphys & mk) == mk) acc += __ldg(trm + 2 * q + 1);\n"
+          << "      }\n      scoef[j] = acc;\n    }\n";
       o << "    __syncthreads();\n";
     }
     // loads (phase 0)
