@@ -263,6 +263,43 @@ static void fuse_ops(std::vector<POp>& ops, int fuse_cap) {
   ops.swap(out);
 }
 
+// Inside a pass, a phase monomial commutes with every dense op whose targets
+// it does not touch (controls do not matter: a diagonal on the control commutes
+// with the control projector).  Move each monomial forward into the furthest
+// later diagonal group it can reach, so groups merge and fewer per-thread
+// sincos are needed (the diagonal detector's commutation, Alg. 8, applied at
+// monomial granularity inside a pass).
+static void sink_monomials(std::vector<POp>& ops) {
+  for (size_t i = 0; i < ops.size(); i++) {
+    if (ops[i].type != POp::DIAG) continue;
+    std::vector<Mono> keep;
+    for (const Mono& m : ops[i].mono) {
+      size_t dest = i;
+      for (size_t j = i + 1; j < ops.size(); j++) {
+        if (ops[j].type == POp::DIAG) {
+          dest = j;
+          continue;
+        }
+        u64 tm = 0;
+        for (int pos : ops[j].tpos) tm |= 1ull << pos;
+        if (m.mask & tm) break;
+      }
+      if (dest == i) keep.push_back(m);
+      else ops[dest].mono.push_back(m);
+    }
+    ops[i].mono.swap(keep);
+  }
+  std::vector<POp> out;
+  for (POp& op : ops) {
+    if (op.type == POp::DIAG) {
+      merge_mono(op.mono);
+      if (op.mono.empty()) continue;
+    }
+    out.push_back(std::move(op));
+  }
+  ops.swap(out);
+}
+
 // Assign register layouts ("phases") to the dense ops of a chunk pass.
 static void assign_phases(PassPlan& p) {
   const int m = (int)p.cpos.size();
@@ -312,6 +349,7 @@ static void finalize_chunk_pass(Sched& S, PassPlan& p, u64 need_pos, int nl) {
   p.opos = p.cpos;
   for (POp& op : p.ops)
     if (op.type == POp::DIAG) merge_mono(op.mono);
+  if (S.cfg->flags & QS_OPT_DIAG) sink_monomials(p.ops);
   bool all_diag = true;
   for (const POp& op : p.ops)
     if (op.type != POp::DIAG) all_diag = false;

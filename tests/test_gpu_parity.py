@@ -225,6 +225,58 @@ def test_launch_count_and_timing(qs):
     s.close()
 
 
+def test_wide_gates_small_state(qs):
+    """5- and 6-target unitaries / diagonals (QS_MAX_TARGETS) on <= 12-qubit
+    shards (SMALL kernel) vs the oracle."""
+    rng = np.random.default_rng(21)
+    n = 11
+    gates = [W.Gate("UNITARY", tuple(int(q) for q in rng.permutation(n)[:6]), (), (), W.haar_unitary(64, rng)),
+             W.Gate("DIAGONAL", tuple(int(q) for q in rng.permutation(n)[:6]), (), (), W.random_phases(64, rng)),
+             W.Gate("UNITARY", (1, 3, 5, 7, 9), (0,), (), W.haar_unitary(32, rng))]
+    gates = W.random_circuit(n, 40, 3) + gates + W.random_circuit(n, 40, 4)
+    psi, _ = sim_run(qs, n, gates, basis=9)
+    assert maxdiff(psi, oracle.apply_circuit(n, gates, x=9)) < TOL
+
+
+def test_wide_gate_large_state_unsupported(qs):
+    rng = np.random.default_rng(2)
+    s = qs.Simulator(16)
+    with pytest.raises(qs.QSError) as e:
+        s.apply([W.Gate("UNITARY", (0, 3, 7, 11), (), (), W.haar_unitary(16, rng))])
+    assert e.value.code == qs.QS_EUNSUPPORTED
+    s.close()
+
+
+@pytest.mark.parametrize("n", [12, 13])
+def test_small_kernel_boundary(qs, n):
+    """nl = 12 runs the SMALL kernel, nl = 13 the chunk kernels."""
+    gates = W.random_circuit(n, 150, 30 + n, diag_bias=0.3)
+    psi, st = sim_run(qs, n, gates, basis=1)
+    assert maxdiff(psi, oracle.apply_circuit(n, gates, x=1)) < TOL
+
+
+def test_empty_circuit_sharded(qs):
+    psi, _ = sim_run(qs, 10, [], basis=1000, ranks=4)
+    want = np.zeros(1 << 10, dtype=complex)
+    want[1000] = 1
+    assert np.array_equal(psi, want)
+
+
+def test_qft33_single_gpu_max_size(qs):
+    """Largest single-B200 size (128 GiB state): QFT-33 closed form, sampled."""
+    n = 33
+    x = 0x1F2E3D4C5 % (1 << n)
+    s = qs.Simulator(n)
+    s.set_basis_state(x)
+    s.apply(W.qft(n))
+    for off in (0, (1 << n) // 2 + 12345, (1 << n) - 2048):
+        got = s.state(int(off), 2048)
+        k = np.arange(int(off), int(off) + 2048, dtype=np.int64)
+        want = np.exp(2j * math.pi * ((x * k) % (1 << n)) / (1 << n)) / math.sqrt(1 << n)
+        assert maxdiff(got, want) < 1e-12
+    s.close()
+
+
 # ------------------------------------------------------------ bench configuration
 
 def test_qft30_sampled_closed_form(qs):

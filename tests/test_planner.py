@@ -158,6 +158,32 @@ def test_plan_shapes_large():
     assert p["stats"]["n_passes"] >= 1
 
 
+@pytest.mark.parametrize("n", [1, 2, 12, 13])
+def test_replay_size_boundaries(n):
+    gates = W.random_circuit(n, 60, 100 + n, diag_bias=0.3)
+    _, psi = run(n, gates, basis=(1 << n) - 1)
+    assert np.max(np.abs(psi - oracle.apply_circuit(n, gates, x=(1 << n) - 1))) < 1e-11
+
+
+def test_replay_wide_gates_small():
+    rng = np.random.default_rng(4)
+    n = 9
+    gates = [W.Gate("UNITARY", (0, 2, 4, 6, 8, 1), (), (), W.haar_unitary(64, rng)),
+             W.Gate("DIAGONAL", (3, 5, 7, 0, 1), (2,), (), W.random_phases(32, rng))]
+    _, psi = run(n, W.random_circuit(n, 20, 1) + gates)
+    want = oracle.apply_circuit(n, W.random_circuit(n, 20, 1) + gates)
+    assert np.max(np.abs(psi - want)) < 1e-11
+
+
+def test_plan_dims_rejected():
+    with pytest.raises(qs.QSError):
+        qs.plan_json(41, [])
+    with pytest.raises(qs.QSError):
+        qs.plan_json(4, [], n_ranks=3)
+    with pytest.raises(qs.QSError):
+        qs.plan_json(3, [], n_ranks=8)
+
+
 def test_invalid_gates_rejected():
     with pytest.raises(qs.QSError):
         qs.plan_json(3, [W.Gate("H", (3,))])
