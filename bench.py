@@ -46,6 +46,18 @@ def measured_peaks():
         return 6650.0, "fallback"
 
 
+def measured_traffic(workload: str, kernel: str):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)
+    of this workload's dominant kernel from the committed ncu --set full
+    capture (profiles/traffic.json), or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        e = d[workload][kernel]
+        return e["bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def make_circuit(workload: str, n: int):
     import workloads as W
     if workload == "qft":
@@ -246,7 +258,8 @@ def main():
         st = sim.stats()
         plan_ms += st["t_plan_ms"]
         dev_ms += st["t_device_ms"]
-        for k in ("K1_chunk", "K2_dense", "K3_diag", "small", "K5_expand", "K5_merge", "init", "K4_swap"):
+        for k in ("K1_chunk", "K2_dense", "K3_diag", "small", "K5_expand", "K5_merge", "init", "K4_swap",
+                  "substate"):
             t = sim.kernel_timing(k)
             a = kt.setdefault(k, {"launches": 0, "ms": 0.0, "bytes": 0})
             for f in a:
@@ -277,7 +290,8 @@ def main():
         else:
             roof = {"kernel": dom[0], "bound": "hbm", "achieved": ach, "peak": peak,
                     "peak_source": peak_src + " (MEASURED_PEAKS.json hbm_gbs, burst copy)",
-                    "unit": "GB/s", "frac": ach / peak, "traffic": None,
+                    "unit": "GB/s", "frac": ach / peak, "traffic": measured_traffic(
+                        "%s%d" % (args.workload, n), dom[0]),
                     "bytes_per_launch": per_launch, "avg_launch_ms": avg_ms,
                     "share_of_step": dom[1]["ms"] / args.steps / ms}
 

@@ -468,7 +468,7 @@ int execute(qs_ctx* ctx, const Plan& plan) {
             CU(launch_pass(p.kernel, dblob, h, buf, sh.stream));
           }
           ctx->launches++;
-          kind = p.kernel;
+          kind = (p.buf == 0) ? p.kernel : KK_SUB;  // full-state passes only per kernel
           bytes = ((p.src_mode ? 16ull : 32ull) << p.nl);
           break;
         }

@@ -349,7 +349,27 @@ static void finalize_chunk_pass(Sched& S, PassPlan& p, u64 need_pos, int nl) {
   p.opos = p.cpos;
   for (POp& op : p.ops)
     if (op.type == POp::DIAG) merge_mono(op.mono);
-  if (S.cfg->flags & QS_OPT_DIAG) sink_monomials(p.ops);
+  if (S.cfg->flags & QS_OPT_DIAG) {
+    // keep the sunk order only if it lowers the estimated per-thread sincos
+    // count: 1 + (dense-target qubits a group touches) per diagonal group
+    auto est = [](const std::vector<POp>& ops) {
+      u64 T = 0;
+      for (const POp& op : ops)
+        if (op.type == POp::DENSE)
+          for (int pos : op.tpos) T |= 1ull << pos;
+      int c = 0;
+      for (const POp& op : ops)
+        if (op.type == POp::DIAG) {
+          u64 s = 0;
+          for (const Mono& m : op.mono) s |= m.mask;
+          c += 1 + popc(s & T);
+        }
+      return c;
+    };
+    std::vector<POp> sunk = p.ops;
+    sink_monomials(sunk);
+    if (est(sunk) < est(p.ops)) p.ops.swap(sunk);
+  }
   bool all_diag = true;
   for (const POp& op : p.ops)
     if (op.type != POp::DIAG) all_diag = false;

@@ -33,7 +33,8 @@ enum KernelKind {
   KK_INIT = 6,    // basis-state initialisation
   KK_SWAP = 7,    // K4 exchange (NCCL / copies)
   KK_READ = 8,    // K6 readout gather
-  KK_NUM = 9
+  KK_SUB = 9,     // passes on booster sub-states (timing class only)
+  KK_NUM = 10
 };
 
 // Register-op types inside a pass.
