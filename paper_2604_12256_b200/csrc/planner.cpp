@@ -15,6 +15,7 @@
 //                      (Eq. 4).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cmath>
 #include <map>
@@ -418,7 +419,11 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
     // given about the FP64 work the HBM time of a write-only pass covers
     // (~48/amp at 6.5 TB/s and ~18 TFLOP/s FP64), so ALU-heavy work moves to
     // the following read+write passes; other passes are capacity-limited.
-    const double budget = (buf == 0 && S.src_mode && !small) ? 48.0 : 400.0;
+    static const double wo_budget = [] {
+      const char* e = getenv("QS_WO_BUDGET");  // experiment knob
+      return (e && *e) ? atof(e) : 48.0;
+    }();
+    const double budget = (buf == 0 && S.src_mode && !small) ? wo_budget : 400.0;
     double cost = 0;
     size_t n_mono = 0;
     int dense_taken = 0;
