@@ -40,8 +40,11 @@ cudaError_t launch_gather(const double2* state, double2* out, u64 off, u64 count
 bool jit_prepare(const unsigned char* blob, int device, void** fn_out, int* grid_per_sm,
                  size_t* smem_out, std::string& err, bool compile_only);
 cudaError_t jit_launch(void* fn, int grid, size_t smem, const unsigned char* dblob,
-                       double2* state, u64 rank_base, const void* pool_host, size_t pool_bytes,
-                       cudaStream_t st);
+                       double2* state, u64 rank_base, const u64* vtab, const void* pool_host,
+                       size_t pool_bytes, cudaStream_t st);
+int jit_vary_list(const unsigned char* blob, VaryList* v);
+cudaError_t launch_shape_table(const unsigned char* dblob, u64* tab, u64 rank_base, u64 n_chunks,
+                               const VaryList& v, cudaStream_t st);
 size_t jit_param_bytes(const unsigned char* blob);
 void jit_stats(double* compile_ms, uint64_t* compiles, uint64_t* disk_hits);
 std::string jit_source(const unsigned char* blob);
@@ -96,6 +99,8 @@ struct Shard {
   double2* tmp = nullptr;            // readout gather buffer
   size_t tmp_cap = 0;                // amplitudes
   int8_t* dmap = nullptr;            // logical->physical map (device)
+  u64* vtab = nullptr;               // per-chunk shape sums of the running pass
+  size_t vtab_cap = 0;               // entries
   std::vector<Timed> timed;          // per-launch events of the last call
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
@@ -460,7 +465,20 @@ int execute(qs_ctx* ctx, const Plan& plan) {
             if (grid > h.n_chunks) grid = h.n_chunks;
             const unsigned char* hb = blobs[si].data() + blob_off[si][k];
             const size_t pb = jit_param_bytes(hb);
-            CU(jit_launch(fn, (int)grid, smem, dblob, buf, h.rank_base, hb + h.off_pool, pb,
+            VaryList vl;
+            if (jit_vary_list(hb, &vl)) {
+              const size_t need = (size_t)h.n_chunks * vl.n;
+              if (need > sh.vtab_cap) {
+                if (sh.vtab) CU(cudaFree(sh.vtab));
+                sh.vtab = nullptr;
+                sh.vtab_cap = 0;
+                CU(cudaMalloc(&sh.vtab, need * sizeof(u64)));
+                sh.vtab_cap = need;
+              }
+              CU(launch_shape_table(dblob, sh.vtab, h.rank_base, h.n_chunks, vl, sh.stream));
+              ctx->launches++;
+            }
+            CU(jit_launch(fn, (int)grid, smem, dblob, buf, h.rank_base, sh.vtab, hb + h.off_pool, pb,
                           sh.stream));
             ctx->jit_launches++;
           } else {
@@ -658,6 +676,7 @@ void qs_destroy(qs_ctx* ctx) {
     cudaFree(s.subpool);
     cudaFree(s.tmp);
     cudaFree(s.dmap);
+    cudaFree(s.vtab);
     for (cudaEvent_t e : s.ev_pool) cudaEventDestroy(e);
     if (s.t0) cudaEventDestroy(s.t0);
     if (s.t1) cudaEventDestroy(s.t1);

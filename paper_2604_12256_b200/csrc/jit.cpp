@@ -112,6 +112,12 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+// the mbarrier sees one arrival once all of this thread's prior cp.async land
+__device__ __forceinline__ void cp_async_mbar_arrive(u64* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(sa(b)) : "memory");
+}
+// barrier of one 256-thread chunk group (named barrier 1 + group)
+__device__ __forceinline__ void gbar(u32 id) { asm volatile("bar.sync %0, 256;" :: "r"(id) : "memory"); }
 )PRELUDE";
 
 static int host_swz(int c) { return c ^ (((c >> 3) ^ (c >> 6) ^ (c >> 9) ^ (c >> 12)) & 7); }
@@ -148,6 +154,16 @@ struct Gen {
   int n_hoist = 0;
   int max_hoist = 0;
   size_t hz_off = 0;  // byte offset of the hoisted-value slots in shared memory
+  int nthreads = kThreads;  // threads per CTA (chunk groups x 256)
+  // Chunk groups per CTA: multi-layout load passes (compute-heavy between
+  // their load and their store) run two groups over three buffers so a load
+  // is always in flight; the others run one group (two CTAs per SM, one
+  // buffer refilled right after its last read).  QS_JIT_GROUPS=1|2 forces.
+  static int groups_per_cta(bool pipe, int nlay) {
+    const char* e = getenv("QS_JIT_GROUPS");
+    if (e && (atoi(e) == 1 || atoi(e) == 2)) return atoi(e);
+    return (pipe && nlay > 1) ? 2 : 1;
+  }
   Gen(const KPass& hh, const unsigned char* blob)
       : h(hh),
         ops(reinterpret_cast<const KOp*>(blob + hh.off_ops)),
@@ -480,6 +496,9 @@ struct Gen {
     emit_arr("vmap", vbig);
     emit_arr("smap", vsmall);
     emit_arr("cmap", cons);
+    // chunk-dependent shapes read from the per-chunk table (qs_kshape_table)
+    const bool use_vtab = !vary.empty() && (int)vary.size() <= kMaxVaryTab;
+    emit_arr("vlist", vary);
     // Load passes stream their chunks through two shared-memory stages filled
     // by cp.async.bulk (the TMA bulk-copy engine) one chunk ahead.
     const bool pipe = (h.src_mode == 0);
@@ -499,7 +518,7 @@ struct Gen {
     // conflict; for run >= 2 the chunk is instead copied with coalesced
     // per-thread cp.async in linear order into XOR-swizzled slots (the
     // exchange layout), conflict-free on both sides.
-    const bool use_tma = pipe && l >= 5 && low_run(L[0]) <= 1;
+    const bool use_tma = pipe && l >= 5 && low_run(L[0]) <= 1 && !getenv("QS_JIT_NOTMA");
     if (use_tma) {
       o << "__device__ __forceinline__ void issue(const double2* __restrict__ state, u64 chunk, double2* dst, u64* bar, u32 lane) {\n"
         << "  const u64 cb = " << cbexpr << ";\n"
@@ -514,7 +533,7 @@ struct Gen {
     } else if (pipe) {
       // thread t copies chunk elements c = t + 256 i (coalesced 128 B+ runs)
       // into slot swz(c) = swz(t) ^ swz(256 i)
-      o << "__device__ __forceinline__ void issue_async(const double2* __restrict__ state, u64 chunk, double2* stage, u64 tpd, int sd) {\n"
+      o << "__device__ __forceinline__ void issue_async(const double2* __restrict__ state, u64 chunk, double2* stage, u64* bar, u64 tpd, int sd) {\n"
         << "  const u64 cb = " << cbexpr << ";\n"
         << "  const double2* sp = state + (cb | tpd);\n";
       for (int i = 0; i < kNReg; i++) {
@@ -523,57 +542,80 @@ struct Gen {
           if (i >> k & 1) off |= 1ull << h.cpos[kLogT + k];
         o << "  cp_async16(stage + (sd ^ " << host_swz(i << kLogT) << "), sp + " << u(off) << ");\n";
       }
-      o << "  cp_async_commit();\n}\n";
+      o << "  cp_async_mbar_arrive(bar);\n}\n";
     }
-    // One stage per CTA, two CTAs per SM: the refill of the stage with the
-    // next chunk is issued right after the chunk's last shared-memory read,
-    // so it overlaps the last layout's compute + stores and the other CTA.
+    // A CTA runs NG chunk groups of 256 threads; its chunk sequence
+    // k = 0, 1, 2, ... (chunk blockIdx.x + k * gridDim.x) is dealt round-robin
+    // to the groups.  Load passes keep NB = NG + 1 chunk buffers: chunk k
+    // lives in buffer k % NB, and right after its last shared-memory read the
+    // buffer is refilled with chunk k + NB, so a load is in flight while every
+    // group computes.  Write-only passes need a buffer per group only for
+    // their layout exchanges.
+    const int NG = groups_per_cta(pipe, nlay);
+    const int NB = pipe ? (NG == 1 ? 1 : NG + 1) : (xchg ? NG : 0);
+    nthreads = kThreads * NG;
     const size_t npool = (h.total_bytes - h.off_pool) / sizeof(double);
     param_pool = npool > 0 && npool <= kMaxParamPool;
     if (param_pool) o << "struct QsPool { double v[" << npool << "]; };\n";
-    o << "extern \"C\" __global__ void __launch_bounds__(256, 2)\n" << kname
-      << "(const unsigned char* __restrict__ blob, double2* __restrict__ state, u64 rank_base"
+    o << "extern \"C\" __global__ void __launch_bounds__(" << nthreads << ", " << (NG == 1 && NB <= 1 ? 2 : 1)
+      << ")\n" << kname
+      << "(const unsigned char* __restrict__ blob, double2* __restrict__ state, u64 rank_base, "
+         "const u64* __restrict__ vtab"
       << (param_pool ? ", const QsPool P" : "") << ") {\n";
     o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n";
-    const int sch_bytes = (pipe || xchg) ? CH * 16 : 0;
-    o << "  double2* stage = reinterpret_cast<double2*>(smem_raw);\n";
-    o << "  double2* sch = stage;\n";
-    o << "  u64* scoef = reinterpret_cast<u64*>(smem_raw + " << sch_bytes << ");\n";
-    o << "  (void)sch; (void)scoef; (void)stage;\n";
+    const size_t buf_bytes = (size_t)NB * CH * 16;
+    const size_t sc_bytes = ((nsh * 8 + 15) / 16) * 16;
+    o << "  const u32 tid = threadIdx.x & 255u;\n";
+    o << "  const u32 grp = threadIdx.x >> 8;\n  (void)grp;\n";
+    o << "  double2* const bufs = reinterpret_cast<double2*>(smem_raw);\n  (void)bufs;\n";
+    o << "  u64* scoef = reinterpret_cast<u64*>(smem_raw + " << buf_bytes << " + grp * " << sc_bytes << ");\n";
+    o << "  (void)scoef;\n";
+    const size_t mbar_off = buf_bytes + NG * sc_bytes;
+    // issued[b]: loads issued into buffer b so far (two groups: see the wait)
     if (pipe)
-      o << "  u64* mbar = reinterpret_cast<u64*>(smem_raw + " << sch_bytes + ((nsh * 8 + 15) / 16) * 16
-        << ");\n";
-    hz_off = (size_t)sch_bytes + ((nsh * 8 + 15) / 16) * 16 + (pipe ? 16 : 0);
-    // keep 2 CTAs/SM: <= ~110 KB of shared memory per CTA
-    max_hoist = (int)std::max<long>(0, ((long)110 * 1024 - (long)hz_off) / (kThreads * 16));
+      o << "  u64* mbar = reinterpret_cast<u64*>(smem_raw + " << mbar_off << ");\n"
+        << "  volatile u32* issued = reinterpret_cast<volatile u32*>(smem_raw + " << mbar_off + NB * 8
+        << ");\n  (void)issued;\n";
+    hz_off = mbar_off + (pipe ? ((NB * 12 + 15) / 16) * 16 : 0);
+    // hoisted per-thread values (shared by the groups: they depend on tid only)
+    // fill what shared memory is left: 227 KB per SM, minus the 4 KB table
+    const long smem_cap = (NG == 1 && NB <= 1) ? 110 * 1024 : 222 * 1024;
+    max_hoist = (int)std::max<long>(0, (smem_cap - (long)hz_off) / (kThreads * 16));
     if (max_hoist > 24) max_hoist = 24;
     o << "  double2* hz = reinterpret_cast<double2*>(smem_raw + " << hz_off << ");\n  (void)hz;\n";
     o << "  const double* __restrict__ pool = reinterpret_cast<const double*>(blob + " << h.off_pool << ");\n";
     o << "  const int* __restrict__ shp = reinterpret_cast<const int*>(blob + " << h.off_shapes << ");\n";
     o << "  const u64* __restrict__ trm = reinterpret_cast<const u64*>(blob + " << h.off_terms << ");\n";
     o << "  (void)pool; (void)shp; (void)trm;\n";
-    o << "  const u32 tid = threadIdx.x;\n";
     o << "  __shared__ double2 ctab[256];\n"
-      << "  for (int i = (int)tid; i < 256; i += " << kThreads << ") ctab[i] = cis_turns((u64)i << 56);\n"
-      << "  __syncthreads();\n";
+      << "  for (int i = (int)threadIdx.x; i < 256; i += " << nthreads << ") ctab[i] = cis_turns((u64)i << 56);\n";
     for (int p = 0; p < nlay; p++) {
       o << "  const u64 tp" << p << " = " << tphys_expr(p, false) << ";\n";
       if (xchg || (pipe && !use_tma)) o << "  const int st" << p << " = swz(" << tc_expr(p) << ");\n";
     }
     o << "  const u64 tpo = " << tphys_expr(nlay - 1, true) << ";\n";
+    const std::string N = u(h.n_chunks);
+    auto chunk_of = [&](const std::string& k) { return "(blockIdx.x + (u64)(" + k + ") * gridDim.x)"; };
+    if (pipe) {
+      o << "  if (threadIdx.x == 0) {\n"
+        << "    for (int b = 0; b < " << NB << "; b++) { mbar_init(mbar + b, " << (use_tma ? 1 : kThreads)
+        << "); issued[b] = 0u; }\n"
+        << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n  }\n";
+    }
+    o << "  __syncthreads();\n";
     if (use_tma) {
       o << "  const int tcl0 = " << tc_expr(0) << ";\n";
-      o << "  if (tid == 0) { mbar_init(mbar, 1);\n"
-        << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\"); }\n"
-        << "  __syncthreads();\n"
-        << "  if (tid < 32 && blockIdx.x < " << u(h.n_chunks) << ") issue(state, blockIdx.x, stage, mbar, tid);\n"
-        << "  u32 par = 0;\n";
+      o << "  for (u32 k = grp; k < " << NB << "u; k += " << NG << "u)\n"
+        << "    if (tid < 32 && " << chunk_of("k") << " < " << N << ") { issue(state, " << chunk_of("k")
+        << ", bufs + k * " << CH << ", mbar + k, tid); if (tid == 0) issued[k] = 1u; }\n";
     } else if (pipe) {
       std::string tpd = "(0ull";
       for (int i = 0; i < kLogT; i++)
         tpd += " | ((u64)((tid >> " + std::to_string(i) + ") & 1u) << " + std::to_string((int)h.cpos[i]) + ")";
       o << "  const u64 tpd = " << tpd << ");\n  const int sd = swz((int)tid);\n";
-      o << "  if (blockIdx.x < " << u(h.n_chunks) << ") issue_async(state, blockIdx.x, stage, tpd, sd);\n";
+      o << "  for (u32 k = grp; k < " << NB << "u; k += " << NG << "u)\n"
+        << "    if (" << chunk_of("k") << " < " << N << ") { issue_async(state, " << chunk_of("k")
+        << ", bufs + k * " << CH << ", mbar + k, tpd, sd); if (tid == 0) issued[k] = 1u; }\n";
     }
     // level 1, constant shapes: once
     // level 1: one warp per shape, lanes over its terms, shuffle reduction
@@ -599,18 +641,31 @@ struct Gen {
     }
     o << "  double2 a0, a1, a2, a3, a4, a5, a6, a7, a8, a9, a10, a11, a12, a13, a14, a15;\n";
     const size_t loop_pos = o.str().size();  // hoisted code goes here
-    o << "  for (u64 chunk = blockIdx.x; chunk < " << u(h.n_chunks) << "; chunk += gridDim.x) {\n";
+    o << "  for (u32 k = grp;; k += " << NG << "u) {\n"
+      << "    const u64 chunk = " << chunk_of("k") << ";\n"
+      << "    if (chunk >= " << N << ") break;\n";
+    if (pipe) o << "    const u32 kb = k % " << NB << "u;\n    double2* const sch = bufs + kb * " << CH << ";\n";
+    else if (xchg) o << "    double2* const sch = bufs + grp * " << CH << ";\n";
+    const std::string nxt = chunk_of("k + " + std::to_string(NB));
+    const std::string count = "if (tid == 0) { __threadfence_block(); issued[kb] = k / " +
+                              std::to_string(NB) + "u + 2u; }";
     const std::string refill =
-        use_tma ? "    __syncthreads();  // every thread is done reading the stage\n"
-                  "    if (tid < 32 && chunk + gridDim.x < " + u(h.n_chunks) +
-                  ") { fence_proxy_async(); issue(state, chunk + gridDim.x, stage, mbar, tid); }\n"
-                : "    __syncthreads();  // every thread is done reading the stage\n"
-                  "    if (chunk + gridDim.x < " + u(h.n_chunks) +
-                  ") issue_async(state, chunk + gridDim.x, stage, tpd, sd);\n";
+        use_tma ? "    gbar(1u + grp);  // every thread is done reading the buffer\n"
+                  "    if (tid < 32 && " + nxt + " < " + N +
+                  ") { fence_proxy_async(); issue(state, " + nxt + ", sch, mbar + kb, tid); " + count + " }\n"
+                : "    gbar(1u + grp);  // every thread is done reading the buffer\n"
+                  "    if (" + nxt + " < " + N + ") { issue_async(state, " + nxt + ", sch, mbar + kb, tpd, sd); " +
+                  count + " }\n";
     o << "    const u64 cb = " << cbexpr << ";\n";
     o << "    const u64 cphys = cb | rank_base;\n    (void)cphys;\n";
-    if (!vary.empty()) {
-      o << "    __syncthreads();\n";
+    if (use_vtab) {
+      // one coalesced row per chunk instead of the level-1 term loops
+      o << "    gbar(1u + grp);\n"
+        << "    if (tid < " << vary.size() << "u) scoef[vlist[tid]] = __ldg(vtab + chunk * " << vary.size()
+        << "ull + tid);\n"
+        << "    gbar(1u + grp);\n";
+    } else if (!vary.empty()) {
+      o << "    gbar(1u + grp);\n";
       if (!vbig.empty()) level1("vmap", vbig.size(), true);
       if (!vsmall.empty())
         o << "    for (int jj = (int)tid; jj < " << vsmall.size() << "; jj += " << kThreads << ") {\n"
@@ -621,7 +676,7 @@ struct Gen {
           << "        const u64 mk = __ldg(trm + 2 * q);\n"
           << "        if ((cphys & mk) == mk) acc += __ldg(trm + 2 * q + 1);\n"
           << "      }\n      scoef[j] = acc;\n    }\n";
-      o << "    __syncthreads();\n";
+      o << "    gbar(1u + grp);\n";
     }
     // loads (phase 0)
     for (int r = 0; r < kNReg; r++) nm[r] = r;
@@ -671,8 +726,14 @@ struct Gen {
       o << "    }\n";
     } else {
       // staged chunk (linear chunk-index layout) -> registers of layout 0
+      // The j-th use of buffer b (chunk k = j * NB + b) is its mbarrier's
+      // phase j.  With two groups, phase j - 1 belongs to the other group and
+      // may still be in flight, and a parity wait on j would then alias to the
+      // completed phase j - 2.  The load of phase j is issued only after phase
+      // j - 1 was consumed, so first wait until it has been issued.
+      if (NG > 1) o << "    while (issued[kb] < k / " << NB << "u + 1u) {}\n";
+      o << "    mbar_wait(mbar + kb, (k / " << NB << "u) & 1u);\n";
       if (use_tma) {
-        o << "    mbar_wait(mbar, par); par ^= 1u;\n";
         for (int r = 0; r < kNReg; r++) {
           int rc = 0;
           for (int k = 0; k < kRegBits; k++)
@@ -680,17 +741,16 @@ struct Gen {
           o << "    " << A(r) << " = sch[tcl0 | " << rc << "];\n";
         }
       } else {
-        o << "    cp_async_wait_all();\n    __syncthreads();  // every thread's copies have landed\n";
         for (int r = 0; r < kNReg; r++) o << "    " << A(r) << " = sch[st0 ^ " << reg_slot(0, r) << "];\n";
       }
       if (nlay == 1) o << refill;
     }
     for (int p = 0; p < nlay; p++) {
       if (p > 0) {
-        o << "    __syncthreads();\n";
+        o << "    gbar(1u + grp);\n";
         for (int r = 0; r < kNReg; r++)
           o << "    sch[st" << p - 1 << " ^ " << reg_slot(p - 1, r) << "] = " << A(r) << ";\n";
-        o << "    __syncthreads();\n";
+        o << "    gbar(1u + grp);\n";
         for (int r = 0; r < kNReg; r++)
           o << "    " << A(r) << " = sch[st" << p << " ^ " << reg_slot(p, r) << "];\n";
         if (pipe && p == nlay - 1) o << refill;
@@ -713,7 +773,7 @@ struct Gen {
       o << "      so[" << u(reg_phys(nlay - 1, r, true)) << "] = " << A(r) << ";\n";
     o << "    }\n  }\n}\n";
     std::string s = o.str();
-    s.insert(loop_pos, pre.str());
+    if (n_hoist) s.insert(loop_pos, "  if (grp == 0) {\n" + pre.str() + "  }\n  __syncthreads();\n");
     return s;
   }
 };
@@ -763,12 +823,14 @@ Driver& driver() {
 
 struct Compiled {
   CUfunction f = nullptr;
+  int threads = kThreads;
   int blocks_per_sm = 1;
   size_t smem = 0;
 };
 
 std::mutex g_mu;
 std::unordered_map<u64, Compiled> g_cache;  // key: hash ^ device
+std::unordered_map<void*, int> g_threads;   // function -> threads per CTA
 double g_compile_ms = 0;
 uint64_t g_compiles = 0, g_disk_hits = 0;
 
@@ -821,12 +883,13 @@ const char* jit_kernel_name(int kernel) {
   }
 }
 
-std::string jit_source(const unsigned char* blob, size_t* smem_bytes = nullptr) {
+std::string jit_source(const unsigned char* blob, size_t* smem_bytes = nullptr, int* threads = nullptr) {
   KPass h;
   memcpy(&h, blob, sizeof h);
   Gen g(h, blob);
   std::string s = g.build(jit_kernel_name(h.kernel), h.kernel == KK_CHUNK, h.kernel == KK_DIAG);
   if (smem_bytes) *smem_bytes = g.hz_off + (size_t)g.n_hoist * kThreads * 16;
+  if (threads) *threads = g.nthreads;
   return s;
 }
 
@@ -838,7 +901,8 @@ bool jit_prepare(const unsigned char* blob, int device, void** fn_out, int* grid
   memcpy(&h, blob, sizeof h);
   const char* kname = jit_kernel_name(h.kernel);
   size_t smem = 0;
-  const std::string src = jit_source(blob, &smem);
+  int threads = kThreads;
+  const std::string src = jit_source(blob, &smem, &threads);
   const u64 hash = fnv1a(src);
   std::lock_guard<std::mutex> lk(g_mu);
   const u64 key = hash ^ ((u64)(device + 1) * 0x9E3779B97F4A7C15ull);
@@ -851,6 +915,12 @@ bool jit_prepare(const unsigned char* blob, int device, void** fn_out, int* grid
   }
   char hx[32];
   snprintf(hx, sizeof hx, "%016llx", (unsigned long long)hash);
+  if (const char* dd = getenv("QS_JIT_DUMP")) {  // debugging: keep the generated source
+    if (FILE* w = fopen((std::string(dd) + "/" + hx + "_" + kname + ".cu").c_str(), "wb")) {
+      fwrite(src.data(), 1, src.size(), w);
+      fclose(w);
+    }
+  }
   const std::string dir = cache_dir();
   const std::string path = dir + "/" + hx + ".cubin";
   std::vector<char> cubin;
@@ -896,10 +966,12 @@ bool jit_prepare(const unsigned char* blob, int device, void** fn_out, int* grid
   }
   if (smem > 48 * 1024) d.setattr(c.f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
   int nb = 1;
-  if (d.occ(&nb, c.f, kThreads, smem) != CUDA_SUCCESS || nb < 1) nb = 1;
+  if (d.occ(&nb, c.f, threads, smem) != CUDA_SUCCESS || nb < 1) nb = 1;
   c.blocks_per_sm = nb;
   c.smem = smem;
+  c.threads = threads;
   g_cache[key] = c;
+  g_threads[(void*)c.f] = threads;
   *fn_out = (void*)c.f;
   *grid_per_sm = nb;
   *smem_out = smem;
@@ -915,13 +987,39 @@ size_t jit_param_bytes(const unsigned char* blob) {
   return (npool > 0 && npool <= kMaxParamPool) ? npool * sizeof(double) : 0;
 }
 
+// The chunk-dependent shapes whose level-1 sums the specialised kernel reads
+// from a per-chunk table (qs_kshape_table); 0: none, or too many (the kernel
+// then sums them itself).
+int jit_vary_list(const unsigned char* blob, VaryList* v) {
+  KPass h;
+  memcpy(&h, blob, sizeof h);
+  const KShape* shapes = reinterpret_cast<const KShape*>(blob + h.off_shapes);
+  const KTerm* terms = reinterpret_cast<const KTerm*>(blob + h.off_terms);
+  v->n = 0;
+  for (int j = 0; j < h.n_shapes; j++) {
+    bool var = false;
+    for (int q = shapes[j].term_begin; q < shapes[j].term_end; q++)
+      if (terms[q].ncmask) var = true;
+    if (!var) continue;
+    if (v->n == kMaxVaryTab) return v->n = 0;
+    v->j[v->n++] = (int16_t)j;
+  }
+  return v->n;
+}
+
 cudaError_t jit_launch(void* fn, int grid, size_t smem, const unsigned char* dblob,
-                       double2* state, u64 rank_base, const void* pool_host, size_t pool_bytes,
-                       cudaStream_t st) {
+                       double2* state, u64 rank_base, const u64* vtab, const void* pool_host,
+                       size_t pool_bytes, cudaStream_t st) {
   Driver& d = driver();
-  void* args[] = {(void*)&dblob, (void*)&state, (void*)&rank_base, (void*)pool_host};
-  if (!pool_bytes) args[3] = nullptr;
-  CUresult r = d.launch((CUfunction)fn, (unsigned)grid, 1, 1, kThreads, 1, 1, (unsigned)smem,
+  int threads = kThreads;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_threads.find(fn);
+    if (it != g_threads.end()) threads = it->second;
+  }
+  void* args[] = {(void*)&dblob, (void*)&state, (void*)&rank_base, (void*)&vtab, (void*)pool_host};
+  if (!pool_bytes) args[4] = nullptr;
+  CUresult r = d.launch((CUfunction)fn, (unsigned)grid, 1, 1, (unsigned)threads, 1, 1, (unsigned)smem,
                         (CUstream)st, args, nullptr);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorLaunchFailure;
 }

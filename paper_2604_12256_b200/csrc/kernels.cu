@@ -728,6 +728,39 @@ cudaError_t launch_merge(double2* dst, const double2* A, int la, const double2* 
   return cudaGetLastError();
 }
 
+// Level-1 sums of a pass's chunk-dependent shapes for every chunk:
+// tab[c * n + t] = sum of the coefficients of shape v.j[t]'s terms whose
+// non-chunk mask is set in chunk c's physical base (the same sum the
+// interpreter computes per chunk in shared memory).
+__global__ void qs_kshape_table(const unsigned char* __restrict__ blob, u64* __restrict__ tab,
+                                u64 rank_base, VaryList v) {
+  const KPass& P = *reinterpret_cast<const KPass*>(blob);
+  const KShape* S = reinterpret_cast<const KShape*>(blob + P.off_shapes);
+  const KTerm* T = reinterpret_cast<const KTerm*>(blob + P.off_terms);
+  const u64 total = P.n_chunks * (u64)v.n;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (u64)gridDim.x * blockDim.x) {
+    const u64 c = i / (u64)v.n;
+    const int j = v.j[(int)(i - c * (u64)v.n)];
+    const u64 cphys = deposit_runs(P, c) | rank_base;
+    u64 acc = 0;
+    for (int q = S[j].term_begin; q < S[j].term_end; q++) {
+      const u64 mk = T[q].ncmask;
+      if ((cphys & mk) == mk) acc += T[q].coeff;
+    }
+    tab[i] = acc;
+  }
+}
+
+cudaError_t launch_shape_table(const unsigned char* dblob, u64* tab, u64 rank_base, u64 n_chunks,
+                               const VaryList& v, cudaStream_t st) {
+  u64 blocks = (n_chunks * (u64)v.n + 255) / 256;
+  u64 cap = (u64)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks == 0) blocks = 1;
+  qs_kshape_table<<<(unsigned)blocks, 256, 0, st>>>(dblob, tab, rank_base, v);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_set_one(double2* dst, u64 idx, cudaStream_t st) {
   qs_kset_one<<<1, 1, 0, st>>>(dst, idx);
   return cudaGetLastError();

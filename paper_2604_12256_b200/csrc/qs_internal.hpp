@@ -21,6 +21,7 @@ constexpr int kMaxPhases = 8;             // register layouts per chunk pass
 constexpr int kMaxShapes = 1024;          // diag shapes per pass (smem)
 constexpr int kMaxRuns = 16;              // runs of the chunk-id deposit
 constexpr int kMaxExpand = 4;             // sub-states multiplied by K5
+constexpr int kMaxVaryTab = 64;           // chunk-dependent shapes read from a table
 
 // Kernel kinds (stats / timing ids).
 enum KernelKind {
@@ -127,6 +128,13 @@ struct KPass {
   KExpand expand;
   uint32_t off_ops, off_groups, off_shapes, off_terms, off_pool;
   uint32_t total_bytes;
+};
+
+// Chunk-dependent diagonal shapes of a specialised pass whose per-chunk level-1
+// sums are precomputed into a table (row per chunk, column per listed shape).
+struct VaryList {
+  int32_t n;
+  int16_t j[kMaxVaryTab];
 };
 
 }  // namespace qs
