@@ -44,6 +44,9 @@ typedef unsigned int u32;
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {  // a * conj(b)
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
 __device__ __forceinline__ double2 cmac(double2 acc, double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, fma(-a.y, b.y, acc.x)),
                       fma(a.x, b.y, fma(a.y, b.x, acc.y)));
@@ -155,6 +158,9 @@ struct Gen {
   int max_hoist = 0;
   size_t hz_off = 0;  // byte offset of the hoisted-value slots in shared memory
   int nthreads = kThreads;  // threads per CTA (chunk groups x 256)
+  int n_table = 0;          // sincos evaluations left in the loop (need the table)
+  bool hoist_capped = false;  // a loop-invariant sincos did not fit in smem
+  bool table_free = false;    // generation assumes no table: 4 KB more for hoists
   // Chunk groups per CTA: multi-layout load passes (compute-heavy between
   // their load and their store) run two groups over three buffers so a load
   // is always in flight; the others run one group (two CTAs per SM, one
@@ -387,12 +393,19 @@ struct Gen {
     };
     // Hoisted values live in per-thread shared-memory slots (registers are
     // the scarce resource: keeping them live across the loop spills).
+    // (computed once per thread: the table-free sincos; the 256-entry table,
+    // whose random lookups cost shared-memory bank conflicts, is only
+    // instantiated for the sincos left inside the chunk loop)
     auto evar = [&](int R) -> std::string {
-      if (slot_const(R) && n_hoist < max_hoist) {
-        const std::string slot = "hz[" + std::to_string(n_hoist++ * kThreads) + " + tid]";
-        pre << "  " << slot << " = cis_tab(" << shape_sum(G, R) << ", ctab);\n";
-        return slot;
+      if (slot_const(R)) {
+        if (n_hoist < max_hoist) {
+          const std::string slot = "hz[" + std::to_string(n_hoist++ * kThreads) + " + tid]";
+          pre << "  " << slot << " = cis_turns(" << shape_sum(G, R) << ");\n";
+          return slot;
+        }
+        hoist_capped = true;
       }
+      n_table++;
       return "cis_tab(" + shape_sum(G, R) + ", ctab)";
     };
     if (hc) {
@@ -405,20 +418,41 @@ struct Gen {
         pend_scale = false;
       }
     }
+    std::vector<int> lb;  // active register bits
     for (int k = 0; k < kRegBits; k++)
-      if (L >> k & 1) o << "    const double2 E" << k + 1 << " = " << evar(1 << k) << ";\n";
-    for (int r = 0; r < kNReg; r++) {
-      if (!(op.rcm >> r & 1)) continue;
-      std::vector<std::string> f;
-      if (hc) f.push_back("E0");
-      for (int k = 0; k < kRegBits; k++)
-        if ((L >> k & 1) && (r >> k & 1)) f.push_back("E" + std::to_string(k + 1));
-      if (G.ck_off >= 0)
-        f.push_back("make_double2(" + pv(G.ck_off + 2 * r) + ", " + pv(G.ck_off + 2 * r + 1) + ")");
-      if (f.empty()) continue;
-      std::string g = f[0];
-      for (size_t i = 1; i < f.size(); i++) g = "cmul(" + g + ", " + f[i] + ")";
-      o << "    " << A(r) << " = cmul(" << A(r) << ", " << g << ");\n";
+      if (L >> k & 1) {
+        lb.push_back(k);
+        o << "    const double2 E" << k + 1 << " = " << evar(1 << k) << ";\n";
+      }
+    // Register r takes E0 * prod_{k in r & L} E_{k+1} * CK[r].  The products
+    // over subsets of L are walked in Gray-code order -- one running factor,
+    // one multiplication (by E or conj E) per step -- so only F and the E's
+    // are live instead of a tree of partial products.
+    bool fid = !hc;  // F is still the identity
+    if (hc) o << "    double2 F = E0;\n";
+    else o << "    double2 F;\n";
+    const int m = (int)lb.size();
+    for (int i = 0; i < (1 << m); i++) {
+      const int g = i ^ (i >> 1);
+      if (i > 0) {
+        const int b = __builtin_ctz(g ^ ((i - 1) ^ ((i - 1) >> 1)));
+        const std::string e = "E" + std::to_string(lb[b] + 1);
+        if (fid) o << "    F = " << e << ";\n", fid = false;
+        else o << "    F = " << ((g >> b & 1) ? "cmul" : "cmulc") << "(F, " << e << ");\n";
+      }
+      int s = 0;
+      for (int t = 0; t < m; t++)
+        if (g >> t & 1) s |= 1 << lb[t];
+      for (int r = 0; r < kNReg; r++) {
+        if (!(op.rcm >> r & 1) || (r & L) != s) continue;
+        const bool ck = G.ck_off >= 0;
+        const std::string c =
+            ck ? "make_double2(" + pv(G.ck_off + 2 * r) + ", " + pv(G.ck_off + 2 * r + 1) + ")" : "";
+        if (fid && !ck) continue;
+        if (fid) o << "    " << A(r) << " = cmul(" << A(r) << ", " << c << ");\n";
+        else if (!ck) o << "    " << A(r) << " = cmul(" << A(r) << ", F);\n";
+        else o << "    " << A(r) << " = cmul(cmul(" << A(r) << ", F), " << c << ");\n";
+      }
     }
     o << "  }\n";
   }
@@ -435,6 +469,7 @@ struct Gen {
       if (S & ~act) continue;
       if (S == 0 && !op.has_const) continue;
       o << "    { const double2 e = cis_tab(g" << S << ", ctab);\n";
+      n_table++;
       for (int r = 0; r < kNReg; r++)
         if ((r & act) == S) o << "      " << A(r) << " = cmul(" << A(r) << ", e);\n";
       o << "    }\n";
@@ -564,12 +599,16 @@ struct Gen {
       << (param_pool ? ", const QsPool P" : "") << ") {\n";
     o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n";
     const size_t buf_bytes = (size_t)NB * CH * 16;
-    const size_t sc_bytes = ((nsh * 8 + 15) / 16) * 16;
+    // shape sums; with the per-chunk table, two copies: the chunk's and the
+    // group's next chunk's (prefetched during the chunk)
+    const size_t sc_pad = ((nsh * 8 + 15) / 16) * 16;
+    const size_t sc_bytes = use_vtab ? 2 * sc_pad : sc_pad;
+    const std::string SCN = std::to_string(sc_pad / 8);
     o << "  const u32 tid = threadIdx.x & 255u;\n";
     o << "  const u32 grp = threadIdx.x >> 8;\n  (void)grp;\n";
     o << "  double2* const bufs = reinterpret_cast<double2*>(smem_raw);\n  (void)bufs;\n";
-    o << "  u64* scoef = reinterpret_cast<u64*>(smem_raw + " << buf_bytes << " + grp * " << sc_bytes << ");\n";
-    o << "  (void)scoef;\n";
+    o << "  u64* const scbase = reinterpret_cast<u64*>(smem_raw + " << buf_bytes << " + grp * " << sc_bytes << ");\n";
+    o << "  u64* scoef = scbase;\n  (void)scoef;\n";
     const size_t mbar_off = buf_bytes + NG * sc_bytes;
     // issued[b]: loads issued into buffer b so far (two groups: see the wait)
     if (pipe)
@@ -578,8 +617,10 @@ struct Gen {
         << ");\n  (void)issued;\n";
     hz_off = mbar_off + (pipe ? ((NB * 12 + 15) / 16) * 16 : 0);
     // hoisted per-thread values (shared by the groups: they depend on tid only)
-    // fill what shared memory is left: 227 KB per SM, minus the 4 KB table
-    const long smem_cap = (NG == 1 && NB <= 1) ? 110 * 1024 : 222 * 1024;
+    // fill what shared memory is left: 227 KB per CTA (two CTAs per SM: half
+    // of 228 KB, less the per-CTA reservation), minus the 4 KB sincos table
+    // unless no sincos is left inside the loop (second generation pass)
+    const long smem_cap = ((NG == 1 && NB <= 1) ? 113 * 1024 : 227 * 1024) - (table_free ? 0 : 4096);
     max_hoist = (int)std::max<long>(0, (smem_cap - (long)hz_off) / (kThreads * 16));
     if (max_hoist > 24) max_hoist = 24;
     o << "  double2* hz = reinterpret_cast<double2*>(smem_raw + " << hz_off << ");\n  (void)hz;\n";
@@ -587,8 +628,7 @@ struct Gen {
     o << "  const int* __restrict__ shp = reinterpret_cast<const int*>(blob + " << h.off_shapes << ");\n";
     o << "  const u64* __restrict__ trm = reinterpret_cast<const u64*>(blob + " << h.off_terms << ");\n";
     o << "  (void)pool; (void)shp; (void)trm;\n";
-    o << "  __shared__ double2 ctab[256];\n"
-      << "  for (int i = (int)threadIdx.x; i < 256; i += " << nthreads << ") ctab[i] = cis_turns((u64)i << 56);\n";
+    const size_t ctab_pos = o.str().size();  // the sincos table goes here if used
     for (int p = 0; p < nlay; p++) {
       o << "  const u64 tp" << p << " = " << tphys_expr(p, false) << ";\n";
       if (xchg || (pipe && !use_tma)) o << "  const int st" << p << " = swz(" << tc_expr(p) << ");\n";
@@ -632,13 +672,18 @@ struct Gen {
         o << "        acc += __ldg(trm + 2 * q + 1);\n";
       o << "      }\n"
         << "      for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);\n"
-        << "      if ((tid & 31u) == 0) scoef[j] = acc;\n    }\n";
+        << "      if ((tid & 31u) == 0) { scoef[j] = acc;" << (use_vtab && !use_cphys ? " scoef[j + " + SCN + "] = acc;" : "")
+        << " }\n    }\n";
     };
     if (!cons.empty()) {
       o << "  {\n";
       level1("cmap", cons.size(), false);
       o << "  }\n  __syncthreads();\n";
     }
+    const std::string NV = std::to_string(vary.size());
+    if (use_vtab)
+      o << "  { const u64 c0 = " << chunk_of("grp") << ";\n    if (tid < " << NV << "u && c0 < " << N
+        << ") scoef[vlist[tid]] = __ldg(vtab + c0 * " << NV << "ull + tid); }\n  __syncthreads();\n";
     o << "  double2 a0, a1, a2, a3, a4, a5, a6, a7, a8, a9, a10, a11, a12, a13, a14, a15;\n";
     const size_t loop_pos = o.str().size();  // hoisted code goes here
     o << "  for (u32 k = grp;; k += " << NG << "u) {\n"
@@ -659,11 +704,13 @@ struct Gen {
     o << "    const u64 cb = " << cbexpr << ";\n";
     o << "    const u64 cphys = cb | rank_base;\n    (void)cphys;\n";
     if (use_vtab) {
-      // one coalesced row per chunk instead of the level-1 term loops
-      o << "    gbar(1u + grp);\n"
-        << "    if (tid < " << vary.size() << "u) scoef[vlist[tid]] = __ldg(vtab + chunk * " << vary.size()
-        << "ull + tid);\n"
-        << "    gbar(1u + grp);\n";
+      // one coalesced table row per chunk instead of the level-1 term loops,
+      // loaded one chunk ahead (stored to the other copy at the chunk's end)
+      o << "    u64* const scoef = scbase + (((k / " << NG << "u) & 1u) ? " << SCN << " : 0);\n"
+        << "    u64* const scnx = scbase + (((k / " << NG << "u) & 1u) ? 0 : " << SCN << ");\n"
+        << "    u64 nxv = 0ull;\n"
+        << "    { const u64 nc = " << chunk_of("k + " + std::to_string(NG)) << ";\n"
+        << "      if (tid < " << NV << "u && nc < " << N << ") nxv = __ldg(vtab + nc * " << NV << "ull + tid); }\n";
     } else if (!vary.empty()) {
       o << "    gbar(1u + grp);\n";
       if (!vbig.empty()) level1("vmap", vbig.size(), true);
@@ -771,9 +818,14 @@ struct Gen {
     o << "    { double2* __restrict__ so = state + (cb | tpo);\n";
     for (int r = 0; r < kNReg; r++)
       o << "      so[" << u(reg_phys(nlay - 1, r, true)) << "] = " << A(r) << ";\n";
-    o << "    }\n  }\n}\n";
+    o << "    }\n";
+    if (use_vtab) o << "    if (tid < " << NV << "u) scnx[vlist[tid]] = nxv;\n    gbar(1u + grp);\n";
+    o << "  }\n}\n";
     std::string s = o.str();
     if (n_hoist) s.insert(loop_pos, "  if (grp == 0) {\n" + pre.str() + "  }\n  __syncthreads();\n");
+    if (n_table)
+      s.insert(ctab_pos, "  __shared__ double2 ctab[256];\n  for (int i = (int)threadIdx.x; i < 256; i += " +
+                             std::to_string(nthreads) + ") ctab[i] = cis_turns((u64)i << 56);\n");
     return s;
   }
 };
@@ -886,10 +938,26 @@ const char* jit_kernel_name(int kernel) {
 std::string jit_source(const unsigned char* blob, size_t* smem_bytes = nullptr, int* threads = nullptr) {
   KPass h;
   memcpy(&h, blob, sizeof h);
+  const char* kname = jit_kernel_name(h.kernel);
+  const bool multi = h.kernel == KK_CHUNK, diag_only = h.kernel == KK_DIAG;
   Gen g(h, blob);
-  std::string s = g.build(jit_kernel_name(h.kernel), h.kernel == KK_CHUNK, h.kernel == KK_DIAG);
-  if (smem_bytes) *smem_bytes = g.hz_off + (size_t)g.n_hoist * kThreads * 16;
-  if (threads) *threads = g.nthreads;
+  std::string s = g.build(kname, multi, diag_only);
+  // hoists were capped only by the table's 4 KB: if the extra room takes
+  // every loop-invariant sincos out of the loop, no table is needed at all
+  size_t smem = g.hz_off + (size_t)g.n_hoist * kThreads * 16;
+  int nth = g.nthreads;
+  if (g.hoist_capped) {
+    Gen g2(h, blob);
+    g2.table_free = true;
+    std::string s2 = g2.build(kname, multi, diag_only);
+    if (g2.n_table == 0) {
+      s.swap(s2);
+      smem = g2.hz_off + (size_t)g2.n_hoist * kThreads * 16;
+      nth = g2.nthreads;
+    }
+  }
+  if (smem_bytes) *smem_bytes = smem;
+  if (threads) *threads = nth;
   return s;
 }
 

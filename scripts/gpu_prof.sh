@@ -1,9 +1,7 @@
-# GPU tests + a K1 ncu capture (small case) -- one gpurun call
+# full ncu capture of the QFT-30 specialised passes (K2 write-only + K1)
 cd $GRAFT_REPO_ROOT
-timeout 1200 python -m pytest tests -m gpu -q --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
-echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-CMD="python bench.py --n 26 --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0"
+CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 0"
 $CMD > gpurun_out/plain.log 2>&1 && \
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:qs_kpass -s 4 -c 2 \
-  -o gpurun_out/prof_k1 $CMD > gpurun_out/ncu.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:jit -s 2 -c 2 \
+  -o gpurun_out/prof_qft $CMD > gpurun_out/ncu.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/ncu.log
