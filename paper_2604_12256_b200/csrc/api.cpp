@@ -42,9 +42,9 @@ bool jit_prepare(const unsigned char* blob, int device, void** fn_out, int* grid
 cudaError_t jit_launch(void* fn, int grid, size_t smem, const unsigned char* dblob,
                        double2* state, u64 rank_base, const u64* vtab, const void* pool_host,
                        size_t pool_bytes, cudaStream_t st);
-int jit_vary_list(const unsigned char* blob, VaryList* v);
+int jit_table_cols(const unsigned char* blob, TabCols* v);
 cudaError_t launch_shape_table(const unsigned char* dblob, u64* tab, u64 rank_base, u64 n_chunks,
-                               const VaryList& v, cudaStream_t st);
+                               const TabCols& v, cudaStream_t st);
 size_t jit_param_bytes(const unsigned char* blob);
 void jit_stats(double* compile_ms, uint64_t* compiles, uint64_t* disk_hits);
 std::string jit_source(const unsigned char* blob);
@@ -465,9 +465,9 @@ int execute(qs_ctx* ctx, const Plan& plan) {
             if (grid > h.n_chunks) grid = h.n_chunks;
             const unsigned char* hb = blobs[si].data() + blob_off[si][k];
             const size_t pb = jit_param_bytes(hb);
-            VaryList vl;
-            if (jit_vary_list(hb, &vl)) {
-              const size_t need = (size_t)h.n_chunks * vl.n;
+            TabCols vl;
+            if (jit_table_cols(hb, &vl)) {
+              const size_t need = (size_t)h.n_chunks * vl.width;
               if (need > sh.vtab_cap) {
                 if (sh.vtab) CU(cudaFree(sh.vtab));
                 sh.vtab = nullptr;

@@ -26,6 +26,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
+#include <map>
 #include <mutex>
 #include <sstream>
 #include <string>
@@ -133,6 +135,81 @@ static const int kPairA[6] = {0, 0, 0, 1, 1, 2};
 static const int kPairB[6] = {1, 2, 3, 2, 3, 3};
 
 namespace {
+// The per-chunk table of a specialised pass (TabCols).  A diagonal slot (a
+// fast diagonal's E0 or E_k, a sum of shapes) whose chunk-dependent shapes
+// all have an empty thread mask is chunk-only up to a per-thread constant:
+// it becomes a cis column (its sincos is taken once per chunk by the table
+// kernel; the chunk-independent shapes with an empty thread mask are folded
+// in), and its thread-dependent constant shapes are hoisted.  Every other
+// chunk-dependent shape is an angle column.  slot_col: (op index * 32 + R)
+// -> cis column.  false: nothing chunk-dependent, or over the limits.
+bool table_columns(const unsigned char* blob, TabCols* v, std::map<int, int>* slot_col) {
+  KPass h;
+  memcpy(&h, blob, sizeof h);
+  const KOp* ops = reinterpret_cast<const KOp*>(blob + h.off_ops);
+  const KGroup* groups = reinterpret_cast<const KGroup*>(blob + h.off_groups);
+  const KShape* shapes = reinterpret_cast<const KShape*>(blob + h.off_shapes);
+  const KTerm* terms = reinterpret_cast<const KTerm*>(blob + h.off_terms);
+  memset(v, 0, sizeof *v);
+  auto vary = [&](int j) {
+    for (int q = shapes[j].term_begin; q < shapes[j].term_end; q++)
+      if (terms[q].ncmask) return true;
+    return false;
+  };
+  std::vector<int> ang;
+  std::vector<std::vector<int>> cis;
+  const int nph = h.kernel == KK_CHUNK ? h.n_phases : 1;
+  for (int p = 0; p < nph; p++)
+    for (int i = h.phases[p].op_begin; i < h.phases[p].op_end; i++) {
+      const KOp& op = ops[i];
+      if (op.type == OP_DIAG) {
+        const KGroup& G = groups[op.data];
+        for (int j = G.rbeg[0]; j < G.rbeg[kNReg]; j++)
+          if (vary(j)) ang.push_back(j);
+      } else if (op.type == OP_DIAGF) {
+        const KGroup& G = groups[op.data];
+        std::vector<int> slots;
+        if (op.has_const) slots.push_back(0);
+        for (int k = 0; k < kRegBits; k++)
+          if (op.sel >> k & 1) slots.push_back(1 << k);
+        for (int R : slots) {
+          bool any_vary = false, vary_thread = false;
+          for (int j = G.rbeg[R]; j < G.rbeg[R + 1]; j++)
+            if (vary(j)) any_vary = true, vary_thread |= shapes[j].tmask != 0;
+          if (!any_vary) continue;
+          if (vary_thread) {
+            for (int j = G.rbeg[R]; j < G.rbeg[R + 1]; j++)
+              if (vary(j)) ang.push_back(j);
+            continue;
+          }
+          std::vector<int> c;
+          for (int j = G.rbeg[R]; j < G.rbeg[R + 1]; j++)
+            if (vary(j) || shapes[j].tmask == 0) c.push_back(j);
+          if (slot_col) (*slot_col)[i * 32 + R] = (int)cis.size();
+          cis.push_back(c);
+        }
+      }
+    }
+  std::sort(ang.begin(), ang.end());
+  ang.erase(std::unique(ang.begin(), ang.end()), ang.end());
+  if (ang.empty() && cis.empty()) return false;
+  if ((int)ang.size() > kMaxVaryTab || (int)cis.size() > kMaxTabCis) return false;
+  v->n_ang = (int)ang.size();
+  for (size_t t = 0; t < ang.size(); t++) v->ang[t] = (int16_t)ang[t];
+  v->n_cis = (int)cis.size();
+  int nref = 0;
+  for (size_t e = 0; e < cis.size(); e++) {
+    v->cis_beg[e] = (int16_t)nref;
+    for (int j : cis[e]) {
+      if (nref == kMaxTabRefs) return false;
+      v->cis_shape[nref++] = (int16_t)j;
+    }
+  }
+  v->cis_beg[cis.size()] = (int16_t)nref;
+  v->width = ((v->n_ang + 1) & ~1) + 2 * v->n_cis;
+  return true;
+}
+
 struct Gen {
   std::ostringstream o;
   const KPass& h;
@@ -141,6 +218,11 @@ struct Gen {
   const KShape* shapes;
   const KTerm* terms;
   const double* pool;  // host copy of the matrix pool (structure detection)
+  // per-chunk table (qs_kshape_table): columns and diagonal slot -> cis column
+  TabCols tc;
+  std::map<int, int> slot_col;
+  bool use_vtab = false;
+  size_t sc_cis = 0;  // u64 offset of the cis columns in a shape-sum copy
   int nm[kNReg];  // register slot -> variable index (X renames)
   // per-thread factors that multiply every register, not yet applied:
   // folded into the next full-width diagonal's E0, else applied at the store
@@ -158,6 +240,12 @@ struct Gen {
   int max_hoist = 0;
   size_t hz_off = 0;  // byte offset of the hoisted-value slots in shared memory
   int nthreads = kThreads;  // threads per CTA (chunk groups x 256)
+  // fast-diagonal product scheme: 0 two-level, 1 Gray walk (default: best or
+  // tied on QFT/QAOA/diag-chain A/B runs on one box), 2 product tree
+  static int diag_scheme() {
+    const char* e = getenv("QS_JIT_DIAGPROD");
+    return e ? atoi(e) : 1;
+  }
   int n_table = 0;          // sincos evaluations left in the loop (need the table)
   bool hoist_capped = false;  // a loop-invariant sincos did not fit in smem
   bool table_free = false;    // generation assumes no table: 4 KB more for hoists
@@ -178,6 +266,7 @@ struct Gen {
         terms(reinterpret_cast<const KTerm*>(blob + hh.off_terms)),
         pool(reinterpret_cast<const double*>(blob + hh.off_pool)) {
     for (int r = 0; r < kNReg; r++) nm[r] = r;
+    use_vtab = table_columns(blob, &tc, &slot_col);
   }
   std::string A(int r) const { return "a" + std::to_string(nm[r]); }
 
@@ -378,6 +467,18 @@ struct Gen {
     return s;
   }
 
+  std::string shape_sum_list(const std::vector<int>& js) const {
+    std::string s = "0ull";
+    for (int j : js) {
+      const uint32_t tm = shapes[j].tmask;
+      if (tm == 0) s += " + scoef[" + std::to_string(j) + "]";
+      else
+        s += " + (((tid & " + std::to_string(tm) + "u) == " + std::to_string(tm) + "u) ? scoef[" +
+             std::to_string(j) + "] : 0ull)";
+    }
+    return s;
+  }
+
   void diag_fast(const KOp& op) {
     const KGroup& G = groups[op.data];
     const int L = op.sel;
@@ -396,7 +497,26 @@ struct Gen {
     // (computed once per thread: the table-free sincos; the 256-entry table,
     // whose random lookups cost shared-memory bank conflicts, is only
     // instantiated for the sincos left inside the chunk loop)
+    const int opi = (int)(&op - ops);
     auto evar = [&](int R) -> std::string {
+      auto it = use_vtab ? slot_col.find(opi * 32 + R) : slot_col.end();
+      if (it != slot_col.end()) {
+        // chunk part from the table's cis column, times the hoisted
+        // thread-dependent constant part (if any)
+        const std::string cv = "cisv[" + std::to_string(it->second) + "]";
+        std::vector<int> tpart;
+        for (int j = G.rbeg[R]; j < G.rbeg[R + 1]; j++)
+          if (shapes[j].tmask != 0) tpart.push_back(j);
+        if (tpart.empty()) return cv;
+        if (n_hoist < max_hoist) {
+          const std::string slot = "hz[" + std::to_string(n_hoist++ * kThreads) + " + tid]";
+          pre << "  " << slot << " = cis_turns(" << shape_sum_list(tpart) << ");\n";
+          return "cmul(" + slot + ", " + cv + ")";
+        }
+        hoist_capped = true;
+        n_table++;
+        return "cmul(cis_tab(" + shape_sum_list(tpart) + ", ctab), " + cv + ")";
+      }
       if (slot_const(R)) {
         if (n_hoist < max_hoist) {
           const std::string slot = "hz[" + std::to_string(n_hoist++ * kThreads) + " + tid]";
@@ -424,35 +544,111 @@ struct Gen {
         lb.push_back(k);
         o << "    const double2 E" << k + 1 << " = " << evar(1 << k) << ";\n";
       }
-    // Register r takes E0 * prod_{k in r & L} E_{k+1} * CK[r].  The products
-    // over subsets of L are walked in Gray-code order -- one running factor,
-    // one multiplication (by E or conj E) per step -- so only F and the E's
-    // are live instead of a tree of partial products.
-    bool fid = !hc;  // F is still the identity
-    if (hc) o << "    double2 F = E0;\n";
-    else o << "    double2 F;\n";
+    const int scheme = diag_scheme();
+    if (scheme == 1) {
+    // Gray-code walk: one running factor F, one multiplication (by E or
+    // conj E) per step -- minimal live registers, a 2^m - 1 deep chain.
+    {
+      bool fid = !hc;  // F is still the identity
+      if (hc) o << "    double2 F = E0;\n";
+      else o << "    double2 F;\n";
+      const int m = (int)lb.size();
+      for (int i = 0; i < (1 << m); i++) {
+        const int g = i ^ (i >> 1);
+        if (i > 0) {
+          const int b = __builtin_ctz(g ^ ((i - 1) ^ ((i - 1) >> 1)));
+          const std::string e = "E" + std::to_string(lb[b] + 1);
+          if (fid) o << "    F = " << e << ";\n", fid = false;
+          else o << "    F = " << ((g >> b & 1) ? "cmul" : "cmulc") << "(F, " << e << ");\n";
+        }
+        int s = 0;
+        for (int t = 0; t < m; t++)
+          if (g >> t & 1) s |= 1 << lb[t];
+        for (int r = 0; r < kNReg; r++) {
+          if (!(op.rcm >> r & 1) || (r & L) != s) continue;
+          const bool ck = G.ck_off >= 0;
+          const std::string c =
+              ck ? "make_double2(" + pv(G.ck_off + 2 * r) + ", " + pv(G.ck_off + 2 * r + 1) + ")" : "";
+          if (fid && !ck) continue;
+          if (fid) o << "    " << A(r) << " = cmul(" << A(r) << ", " << c << ");\n";
+          else if (!ck) o << "    " << A(r) << " = cmul(" << A(r) << ", F);\n";
+          else o << "    " << A(r) << " = cmul(cmul(" << A(r) << ", F), " << c << ");\n";
+        }
+      }
+    }
+    } else if (scheme == 2) {
+    // Full product tree per register (the compiler shares the prefixes).
+    for (int r = 0; r < kNReg; r++) {
+      if (!(op.rcm >> r & 1)) continue;
+      std::vector<std::string> f;
+      if (hc) f.push_back("E0");
+      for (int k = 0; k < kRegBits; k++)
+        if ((L >> k & 1) && (r >> k & 1)) f.push_back("E" + std::to_string(k + 1));
+      if (G.ck_off >= 0)
+        f.push_back("make_double2(" + pv(G.ck_off + 2 * r) + ", " + pv(G.ck_off + 2 * r + 1) + ")");
+      if (f.empty()) continue;
+      std::string g = f[0];
+      for (size_t i = 1; i < f.size(); i++) g = "cmul(" + g + ", " + f[i] + ")";
+      o << "    " << A(r) << " = cmul(" << A(r) << ", " << g << ");\n";
+    }
+    } else {
+    // Register r takes E0 * prod_{k in r & L} E_{k+1} * CK[r].  Two-level
+    // products: the low half of L's bits gives P_l (all subsets, formed once),
+    // the high half Q_h = E0 * prod (one scope per subset h), and register r
+    // takes Q_h * P_l -- 2-3 cmuls deep (ILP for the FP64 pipe) with only Q_h
+    // and the P_l live (a full product tree keeps up to 15 partial products).
     const int m = (int)lb.size();
-    for (int i = 0; i < (1 << m); i++) {
-      const int g = i ^ (i >> 1);
-      if (i > 0) {
-        const int b = __builtin_ctz(g ^ ((i - 1) ^ ((i - 1) >> 1)));
-        const std::string e = "E" + std::to_string(lb[b] + 1);
-        if (fid) o << "    F = " << e << ";\n", fid = false;
-        else o << "    F = " << ((g >> b & 1) ? "cmul" : "cmulc") << "(F, " << e << ");\n";
+    const int mlo = m / 2;
+    // subset s (bits over lb[0..mlo)) -> expression of P_s ("" = identity)
+    std::vector<std::string> P(1 << mlo);
+    for (int sl = 1; sl < (1 << mlo); sl++) {
+      const int top = 31 - __builtin_clz(sl);
+      const std::string e = "E" + std::to_string(lb[top] + 1);
+      const int rest = sl & ~(1 << top);
+      if (!rest) {
+        P[sl] = e;
+      } else {
+        o << "    const double2 P" << sl << " = cmul(" << P[rest] << ", " << e << ");\n";
+        P[sl] = "P" + std::to_string(sl);
       }
-      int s = 0;
-      for (int t = 0; t < m; t++)
-        if (g >> t & 1) s |= 1 << lb[t];
-      for (int r = 0; r < kNReg; r++) {
-        if (!(op.rcm >> r & 1) || (r & L) != s) continue;
-        const bool ck = G.ck_off >= 0;
-        const std::string c =
-            ck ? "make_double2(" + pv(G.ck_off + 2 * r) + ", " + pv(G.ck_off + 2 * r + 1) + ")" : "";
-        if (fid && !ck) continue;
-        if (fid) o << "    " << A(r) << " = cmul(" << A(r) << ", " << c << ");\n";
-        else if (!ck) o << "    " << A(r) << " = cmul(" << A(r) << ", F);\n";
-        else o << "    " << A(r) << " = cmul(cmul(" << A(r) << ", F), " << c << ");\n";
+    }
+    const bool ck = G.ck_off >= 0;
+    for (int sh = 0; sh < (1 << (m - mlo)); sh++) {
+      o << "    {\n";
+      // Q = E0 * prod of the high bits in sh
+      std::string Q = hc ? "E0" : "";
+      for (int t = 0; t < m - mlo; t++)
+        if (sh >> t & 1) {
+          const std::string e = "E" + std::to_string(lb[mlo + t] + 1);
+          if (Q.empty()) {
+            Q = e;
+          } else {
+            o << "      const double2 Q" << t << " = cmul(" << Q << ", " << e << ");\n";
+            Q = "Q" + std::to_string(t);
+          }
+        }
+      for (int sl = 0; sl < (1 << mlo); sl++) {
+        int s = 0;
+        for (int t = 0; t < mlo; t++)
+          if (sl >> t & 1) s |= 1 << lb[t];
+        for (int t = 0; t < m - mlo; t++)
+          if (sh >> t & 1) s |= 1 << lb[mlo + t];
+        std::string f;
+        if (Q.empty()) f = P[sl];
+        else if (P[sl].empty()) f = Q;
+        else f = "cmul(" + Q + ", " + P[sl] + ")";
+        for (int r = 0; r < kNReg; r++) {
+          if (!(op.rcm >> r & 1) || (r & L) != s) continue;
+          const std::string c =
+              ck ? "make_double2(" + pv(G.ck_off + 2 * r) + ", " + pv(G.ck_off + 2 * r + 1) + ")" : "";
+          if (f.empty() && !ck) continue;
+          if (f.empty()) o << "      " << A(r) << " = cmul(" << A(r) << ", " << c << ");\n";
+          else if (!ck) o << "      " << A(r) << " = cmul(" << A(r) << ", " << f << ");\n";
+          else o << "      " << A(r) << " = cmul(" << A(r) << ", cmul(" << f << ", " << c << "));\n";
+        }
       }
+      o << "    }\n";
+    }
     }
     o << "  }\n";
   }
@@ -532,8 +728,18 @@ struct Gen {
     emit_arr("smap", vsmall);
     emit_arr("cmap", cons);
     // chunk-dependent shapes read from the per-chunk table (qs_kshape_table)
-    const bool use_vtab = !vary.empty() && (int)vary.size() <= kMaxVaryTab;
-    emit_arr("vlist", vary);
+    // destinations in a shape-sum copy of the table row's entries: angle
+    // columns -> their shape's slot, the padding and cis columns -> the cis area
+    const int W = use_vtab ? tc.width : 0;
+    const size_t sc_pad = ((nsh * 8 + 15) / 16) * 16;
+    sc_cis = sc_pad / 8;
+    {
+      std::vector<int> tm;
+      const int apad = (tc.n_ang + 1) & ~1;
+      for (int t = 0; t < W; t++)
+        tm.push_back(t < tc.n_ang ? tc.ang[t] : t < apad ? (int)sc_cis + 2 * tc.n_cis : (int)sc_cis + t - apad);
+      emit_arr("tmap", tm);
+    }
     // Load passes stream their chunks through two shared-memory stages filled
     // by cp.async.bulk (the TMA bulk-copy engine) one chunk ahead.
     const bool pipe = (h.src_mode == 0);
@@ -601,9 +807,9 @@ struct Gen {
     const size_t buf_bytes = (size_t)NB * CH * 16;
     // shape sums; with the per-chunk table, two copies: the chunk's and the
     // group's next chunk's (prefetched during the chunk)
-    const size_t sc_pad = ((nsh * 8 + 15) / 16) * 16;
-    const size_t sc_bytes = use_vtab ? 2 * sc_pad : sc_pad;
-    const std::string SCN = std::to_string(sc_pad / 8);
+    const size_t sc_copy = use_vtab ? sc_pad + (2 * tc.n_cis + 2) * 8 : sc_pad;
+    const size_t sc_bytes = use_vtab ? 2 * sc_copy : sc_copy;
+    const std::string SCN = std::to_string(sc_copy / 8);
     o << "  const u32 tid = threadIdx.x & 255u;\n";
     o << "  const u32 grp = threadIdx.x >> 8;\n  (void)grp;\n";
     o << "  double2* const bufs = reinterpret_cast<double2*>(smem_raw);\n  (void)bufs;\n";
@@ -623,6 +829,7 @@ struct Gen {
     const long smem_cap = ((NG == 1 && NB <= 1) ? 113 * 1024 : 227 * 1024) - (table_free ? 0 : 4096);
     max_hoist = (int)std::max<long>(0, (smem_cap - (long)hz_off) / (kThreads * 16));
     if (max_hoist > 24) max_hoist = 24;
+    if (const char* e = getenv("QS_JIT_MAXHOIST")) max_hoist = std::min(max_hoist, atoi(e));  // experiments
     o << "  double2* hz = reinterpret_cast<double2*>(smem_raw + " << hz_off << ");\n  (void)hz;\n";
     o << "  const double* __restrict__ pool = reinterpret_cast<const double*>(blob + " << h.off_pool << ");\n";
     o << "  const int* __restrict__ shp = reinterpret_cast<const int*>(blob + " << h.off_shapes << ");\n";
@@ -680,10 +887,10 @@ struct Gen {
       level1("cmap", cons.size(), false);
       o << "  }\n  __syncthreads();\n";
     }
-    const std::string NV = std::to_string(vary.size());
+    const std::string NV = std::to_string(W);
     if (use_vtab)
       o << "  { const u64 c0 = " << chunk_of("grp") << ";\n    if (tid < " << NV << "u && c0 < " << N
-        << ") scoef[vlist[tid]] = __ldg(vtab + c0 * " << NV << "ull + tid); }\n  __syncthreads();\n";
+        << ") scoef[tmap[tid]] = __ldg(vtab + c0 * " << NV << "ull + tid); }\n  __syncthreads();\n";
     o << "  double2 a0, a1, a2, a3, a4, a5, a6, a7, a8, a9, a10, a11, a12, a13, a14, a15;\n";
     const size_t loop_pos = o.str().size();  // hoisted code goes here
     o << "  for (u32 k = grp;; k += " << NG << "u) {\n"
@@ -708,6 +915,8 @@ struct Gen {
       // loaded one chunk ahead (stored to the other copy at the chunk's end)
       o << "    u64* const scoef = scbase + (((k / " << NG << "u) & 1u) ? " << SCN << " : 0);\n"
         << "    u64* const scnx = scbase + (((k / " << NG << "u) & 1u) ? 0 : " << SCN << ");\n"
+        << "    const double2* const cisv = reinterpret_cast<const double2*>(scoef + " << sc_cis << ");\n"
+        << "    (void)cisv;\n"
         << "    u64 nxv = 0ull;\n"
         << "    { const u64 nc = " << chunk_of("k + " + std::to_string(NG)) << ";\n"
         << "      if (tid < " << NV << "u && nc < " << N << ") nxv = __ldg(vtab + nc * " << NV << "ull + tid); }\n";
@@ -819,7 +1028,7 @@ struct Gen {
     for (int r = 0; r < kNReg; r++)
       o << "      so[" << u(reg_phys(nlay - 1, r, true)) << "] = " << A(r) << ";\n";
     o << "    }\n";
-    if (use_vtab) o << "    if (tid < " << NV << "u) scnx[vlist[tid]] = nxv;\n    gbar(1u + grp);\n";
+    if (use_vtab) o << "    if (tid < " << NV << "u) scnx[tmap[tid]] = nxv;\n    gbar(1u + grp);\n";
     o << "  }\n}\n";
     std::string s = o.str();
     if (n_hoist) s.insert(loop_pos, "  if (grp == 0) {\n" + pre.str() + "  }\n  __syncthreads();\n");
@@ -1055,24 +1264,10 @@ size_t jit_param_bytes(const unsigned char* blob) {
   return (npool > 0 && npool <= kMaxParamPool) ? npool * sizeof(double) : 0;
 }
 
-// The chunk-dependent shapes whose level-1 sums the specialised kernel reads
-// from a per-chunk table (qs_kshape_table); 0: none, or too many (the kernel
-// then sums them itself).
-int jit_vary_list(const unsigned char* blob, VaryList* v) {
-  KPass h;
-  memcpy(&h, blob, sizeof h);
-  const KShape* shapes = reinterpret_cast<const KShape*>(blob + h.off_shapes);
-  const KTerm* terms = reinterpret_cast<const KTerm*>(blob + h.off_terms);
-  v->n = 0;
-  for (int j = 0; j < h.n_shapes; j++) {
-    bool var = false;
-    for (int q = shapes[j].term_begin; q < shapes[j].term_end; q++)
-      if (terms[q].ncmask) var = true;
-    if (!var) continue;
-    if (v->n == kMaxVaryTab) return v->n = 0;
-    v->j[v->n++] = (int16_t)j;
-  }
-  return v->n;
+// Columns of the per-chunk table of this pass (0: no table -- nothing
+// chunk-dependent, or too much; the kernel then sums the shapes itself).
+int jit_table_cols(const unsigned char* blob, TabCols* v) {
+  return table_columns(blob, v, nullptr) ? v->width : 0;
 }
 
 cudaError_t jit_launch(void* fn, int grid, size_t smem, const unsigned char* dblob,

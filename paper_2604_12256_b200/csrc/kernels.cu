@@ -728,32 +728,48 @@ cudaError_t launch_merge(double2* dst, const double2* A, int la, const double2* 
   return cudaGetLastError();
 }
 
-// Level-1 sums of a pass's chunk-dependent shapes for every chunk:
-// tab[c * n + t] = sum of the coefficients of shape v.j[t]'s terms whose
-// non-chunk mask is set in chunk c's physical base (the same sum the
-// interpreter computes per chunk in shared memory).
+// The per-chunk table of a specialised pass (TabCols, qs_internal.hpp): for
+// every chunk c, the level-1 sums of the listed chunk-dependent shapes (the
+// sum of the coefficients of the shape's terms whose non-chunk mask is set
+// in chunk c's physical base -- what the interpreter computes per chunk in
+// shared memory), and for each cis column exp(2 pi i S / 2^64) of the summed
+// shapes S of one diagonal slot.
+__device__ __forceinline__ u64 shape_level1(const KShape* S, const KTerm* T, int j, u64 cphys) {
+  u64 acc = 0;
+  for (int q = S[j].term_begin; q < S[j].term_end; q++) {
+    const u64 mk = T[q].ncmask;
+    if ((cphys & mk) == mk) acc += T[q].coeff;
+  }
+  return acc;
+}
+
 __global__ void qs_kshape_table(const unsigned char* __restrict__ blob, u64* __restrict__ tab,
-                                u64 rank_base, VaryList v) {
+                                u64 rank_base, TabCols v) {
   const KPass& P = *reinterpret_cast<const KPass*>(blob);
   const KShape* S = reinterpret_cast<const KShape*>(blob + P.off_shapes);
   const KTerm* T = reinterpret_cast<const KTerm*>(blob + P.off_terms);
-  const u64 total = P.n_chunks * (u64)v.n;
+  const int ncol = v.n_ang + v.n_cis;
+  const int apad = (v.n_ang + 1) & ~1;
+  const u64 total = P.n_chunks * (u64)ncol;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (u64)gridDim.x * blockDim.x) {
-    const u64 c = i / (u64)v.n;
-    const int j = v.j[(int)(i - c * (u64)v.n)];
+    const u64 c = i / (u64)ncol;
+    const int t = (int)(i - c * (u64)ncol);
     const u64 cphys = deposit_runs(P, c) | rank_base;
-    u64 acc = 0;
-    for (int q = S[j].term_begin; q < S[j].term_end; q++) {
-      const u64 mk = T[q].ncmask;
-      if ((cphys & mk) == mk) acc += T[q].coeff;
+    u64* row = tab + c * (u64)v.width;
+    if (t < v.n_ang) {
+      row[t] = shape_level1(S, T, v.ang[t], cphys);
+    } else {
+      const int e = t - v.n_ang;
+      u64 th = 0;
+      for (int q = v.cis_beg[e]; q < v.cis_beg[e + 1]; q++) th += shape_level1(S, T, v.cis_shape[q], cphys);
+      reinterpret_cast<double2*>(row + apad)[e] = cis_turns(th);
     }
-    tab[i] = acc;
   }
 }
 
 cudaError_t launch_shape_table(const unsigned char* dblob, u64* tab, u64 rank_base, u64 n_chunks,
-                               const VaryList& v, cudaStream_t st) {
-  u64 blocks = (n_chunks * (u64)v.n + 255) / 256;
+                               const TabCols& v, cudaStream_t st) {
+  u64 blocks = (n_chunks * (u64)(v.n_ang + v.n_cis) + 255) / 256;
   u64 cap = (u64)num_sms() * 8;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;

@@ -130,11 +130,20 @@ struct KPass {
   uint32_t total_bytes;
 };
 
-// Chunk-dependent diagonal shapes of a specialised pass whose per-chunk level-1
-// sums are precomputed into a table (row per chunk, column per listed shape).
-struct VaryList {
-  int32_t n;
-  int16_t j[kMaxVaryTab];
+// Per-chunk table of a specialised pass (qs_kshape_table), one row per chunk:
+//  - angle columns: the level-1 sum of a chunk-dependent shape (u64 turns);
+//  - cis columns: exp(2 pi i sum/2^64) of the summed shapes of one diagonal
+//    slot whose chunk-dependent part does not depend on the thread (a
+//    double2, so the pass takes no sincos for it).
+// Row = n_ang angles, padded to even, then 2 u64 per cis column.
+constexpr int kMaxTabCis = 32;
+constexpr int kMaxTabRefs = 192;
+struct TabCols {
+  int32_t n_ang, n_cis;
+  int16_t ang[kMaxVaryTab];
+  int16_t cis_beg[kMaxTabCis + 1];
+  int16_t cis_shape[kMaxTabRefs];
+  int32_t width;  // u64 per row: ((n_ang + 1) & ~1) + 2 * n_cis
 };
 
 }  // namespace qs
