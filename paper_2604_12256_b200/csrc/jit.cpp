@@ -286,6 +286,18 @@ struct Gen {
       run++;
     }
   }
+  // low_run of the store: consecutive lowest output positions that are
+  // register bits of layout k under the pass's output relabel (opos)
+  int low_run_out(const KPhase& k) const {
+    int run = 0;
+    for (;;) {
+      bool has = false;
+      for (int i = 0; i < kRegBits; i++)
+        if (h.opos[k.reg_c[i]] == h.cpos[run]) has = true;
+      if (!has || run + 1 >= kChunkBits) return run + (has ? 1 : 0);
+      run++;
+    }
+  }
   static KPhase default_layout() {
     KPhase k;
     memset(&k, 0, sizeof k);
@@ -702,7 +714,7 @@ struct Gen {
     L.assign(h.phases, h.phases + nph);
     // >= 4 contiguous amplitudes per thread at the store: lanes would write
     // 64+ B apart; one more exchange to the default layout pays for itself
-    const bool extra_store = low_run(L[nph - 1]) >= 2;
+    const bool extra_store = low_run_out(L[nph - 1]) >= 2;
     if (extra_store) L.push_back(default_layout());
     const int nlay = (int)L.size();
     const bool xchg = nlay > 1;  // any shared-memory exchange

@@ -301,6 +301,26 @@ static void sink_monomials(std::vector<POp>& ops) {
   ops.swap(out);
 }
 
+// Thread-bit order of a register layout: tid bits 0..2 take the lowest
+// non-register chunk bits of distinct residues mod 3 (bank-conflict-free
+// swizzled exchange), then the rest ascending.
+static std::vector<int> phase_thread_order(const std::vector<int>& regs, int m) {
+  std::vector<int> rest;
+  for (int c = 0; c < m; c++)
+    if (std::find(regs.begin(), regs.end(), c) == regs.end()) rest.push_back(c);
+  std::vector<int> order;
+  for (int res = 0; res < 3; res++)
+    for (int c : rest)
+      if (c % 3 == res && std::find(order.begin(), order.end(), c) == order.end()) {
+        order.push_back(c);
+        break;
+      }
+  std::sort(order.begin(), order.end());
+  for (int c : rest)
+    if (std::find(order.begin(), order.end(), c) == order.end()) order.push_back(c);
+  return order;
+}
+
 // Assign register layouts ("phases") to the dense ops of a chunk pass.
 static void assign_phases(PassPlan& p) {
   const int m = (int)p.cpos.size();
@@ -339,7 +359,8 @@ static void assign_phases(PassPlan& p) {
   if (p.kernel != KK_DIAG) p.kernel = (p.phase_regs.size() > 1) ? KK_CHUNK : KK_DENSE;
 }
 
-static void finalize_chunk_pass(Sched& S, PassPlan& p, u64 need_pos, int nl) {
+static void finalize_chunk_pass(Sched& S, PassPlan& p, u64 need_pos, int nl,
+                                std::vector<int>* map) {
   const int m = kChunkBits;
   // chunk positions: the needed ones, filled with the lowest free positions
   u64 c = need_pos;
@@ -377,6 +398,34 @@ static void finalize_chunk_pass(Sched& S, PassPlan& p, u64 need_pos, int nl) {
   p.kernel = all_diag ? KK_DIAG : KK_CHUNK;
   fuse_ops(p.ops, (S.cfg->flags & QS_OPT_FUSE) ? S.cfg->fuse_cap : 1);
   assign_phases(p);
+  // Store relabel (reading r2, virtual qubit map): if the last register
+  // layout holds the lowest chunk bits, each thread would store 2^run
+  // contiguous amplitudes and the lanes would write 64+ B apart.  Instead
+  // the pass writes its output with the chunk bits permuted -- the last
+  // layout's thread bits onto the lowest positions, its register bits on
+  // top -- and the map records where every qubit went (no extra exchange,
+  // coalesced stores).
+  static const bool relabel_on = !getenv("QS_NO_STORE_RELABEL");  // A/B knob
+  if (map && relabel_on) {
+    const std::vector<int>& last = p.phase_regs.back();
+    int run = 0;
+    while (std::find(last.begin(), last.end(), run) != last.end()) run++;
+    if (run >= 2) {
+      std::vector<int> order = phase_thread_order(last, (int)p.cpos.size());
+      order.insert(order.end(), last.begin(), last.end());
+      std::vector<int> opos(p.cpos.size());
+      for (size_t i = 0; i < order.size(); i++) opos[order[i]] = p.cpos[i];
+      std::vector<int>& mp = *map;
+      std::vector<int> moved(mp.size());
+      for (size_t q = 0; q < mp.size(); q++) {
+        moved[q] = mp[q];
+        for (size_t c = 0; c < p.cpos.size(); c++)
+          if (mp[q] == p.cpos[c]) moved[q] = opos[c];
+      }
+      mp.swap(moved);
+      p.opos = opos;
+    }
+  }
   if (S.src_mode && p.buf == 0) {
     p.src_mode = S.src_mode;
     p.exp_bufs = S.exp_bufs;
@@ -507,7 +556,7 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
         p.kernel = KK_SMALL;
         p.cpos.clear();
       } else {
-        finalize_chunk_pass(S, p, need, nl);
+        finalize_chunk_pass(S, p, need, nl, buf == 0 ? &map : nullptr);
       }
       plan.steps.push_back(Step{Step::PASS, p});
       if (buf == 0) {  // statistics count full-state passes only
@@ -874,21 +923,7 @@ int encode_pass(const PassPlan& p, int rank, std::vector<unsigned char>& out, st
       const std::vector<int>& regs = p.phase_regs[ph];
       KPhase& kp = h.phases[ph];
       for (int k = 0; k < kRegBits; k++) kp.reg_c[k] = (int8_t)regs[k];
-      std::vector<int> rest;
-      for (int c = 0; c < m; c++)
-        if (std::find(regs.begin(), regs.end(), c) == regs.end()) rest.push_back(c);
-      // tid bits 0..2: lowest bits of distinct residues mod 3 (bank-conflict
-      // free swizzled exchange), then ascending.
-      std::vector<int> order;
-      for (int res = 0; res < 3; res++)
-        for (int c : rest)
-          if (c % 3 == res && std::find(order.begin(), order.end(), c) == order.end()) {
-            order.push_back(c);
-            break;
-          }
-      std::sort(order.begin(), order.end());
-      for (int c : rest)
-        if (std::find(order.begin(), order.end(), c) == order.end()) order.push_back(c);
+      const std::vector<int> order = phase_thread_order(regs, m);
       for (int i = 0; i < kLogT; i++) kp.thr_c[i] = (int8_t)order[i];
       thr[ph] = order;
     }

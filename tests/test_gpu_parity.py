@@ -69,6 +69,18 @@ def test_random_chunked(qs, n, seed):
 
 
 @pytest.mark.parametrize("jit", [0, 99])
+@pytest.mark.parametrize("n", [16, 20])
+def test_store_relabel(qs, jit, n):
+    """QFT's chunk pass stores through the output relabel (opos != cpos) on
+    both kernel paths; compared with the oracle element by element."""
+    gates = W.qft(n)
+    plan = qs.plan_json(n, gates, basis=9, detail=True)
+    assert any(s["opos"] != s["cpos"] for s in plan["steps"] if s["type"] == "pass" and "opos" in s)
+    psi, _ = sim_run(qs, n, gates, basis=9, jit_min_qubits=jit)
+    assert maxdiff(psi, oracle.apply_circuit(n, gates, x=9)) < TOL
+
+
+@pytest.mark.parametrize("jit", [0, 99])
 @pytest.mark.parametrize("n,seed", [(13, 10), (15, 11), (17, 12)])
 def test_specialised_vs_interpreter_kernels(qs, jit, n, seed):
     """Both kernel paths (NVRTC-specialised per pass: jit_min_qubits=0;

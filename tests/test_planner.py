@@ -133,6 +133,17 @@ def test_replay_qft_closed_form(n):
         assert np.max(np.abs(psi - pins.qft_closed_form(n, x))) < 1e-12
 
 
+@pytest.mark.parametrize("n", [14, 16])
+def test_store_relabel_replay(n):
+    """The last layout of QFT's chunk pass holds the lowest chunk bits: the
+    pass stores with its chunk bits permuted (opos != cpos) and the map
+    records it (reading r2); the replayed result is still the closed form."""
+    plan, psi = run(n, W.qft(n), basis=3)
+    passes = [s for s in plan["steps"] if s["type"] == "pass" and "opos" in s]
+    assert any(s["opos"] != s["cpos"] for s in passes)
+    assert np.max(np.abs(psi - pins.qft_closed_form(n, 3))) < 1e-12
+
+
 def test_replay_qaoa_sharded():
     n = 14
     gates = W.qaoa_maxcut(n, 2, 3)
