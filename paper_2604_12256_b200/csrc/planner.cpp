@@ -476,6 +476,7 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
     double cost = 0;
     size_t n_mono = 0;
     int dense_taken = 0;
+    u64 dense_union = 0;  // dense target positions taken (no-blocking fusion)
     u64 cur_regs = 0;
     int nphase = 1;
     for (size_t gi = 0; gi < rem.size(); gi++) {
@@ -534,9 +535,18 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
           nphase = ph;
           cur_regs = nr;
         }
-        if (!blocking && dense_taken > 0) { stop = true; defer(); continue; }
+        // without cache blocking a pass is one state sweep for one gate -- or,
+        // with fusion, for the gates whose targets fuse into one <= F-qubit
+        // unitary (the paper's Naive_f, L782)
+        if (!blocking && dense_taken > 0 &&
+            (!(S.cfg->flags & QS_OPT_FUSE) || popc(dense_union | tp) > S.cfg->fuse_cap)) {
+          stop = true;
+          defer();
+          continue;
+        }
         need = nn;
         cost += c;
+        dense_union |= tp;
       }
       p.ops.push_back(dense_pop(g, map));
       ++dense_taken;

@@ -29,6 +29,12 @@ def main():
         "cz_chain": [G("CZ", (q + 1,), (q,)) for q in range(n - 1)],
         "rzz_all": W.rzz_full(n, 3, h_layer=False),
         "u3_12": [G("U3", (q,), (), (0.1, 0.2, 0.3)) for q in list(range(5)) + list(range(20, 27))],
+        # QAOA mixer-like passes: RX on k mid qubits (l = 3 low positions + k)
+        "rx9_mid": [G("RX", (q,), (), (0.1 * q,)) for q in range(9, 18)],
+        "rx8_mid": [G("RX", (q,), (), (0.1 * q,)) for q in range(9, 17)],
+        "rx7_mid": [G("RX", (q,), (), (0.1 * q,)) for q in range(9, 16)],
+        "rx4_mid": [G("RX", (q,), (), (0.1 * q,)) for q in range(9, 13)],
+        "h9_mid": [G("H", (q,), ()) for q in range(9, 18)],
     }
     sim = qs.Simulator(n)
     sim.apply([G("H", (q,)) for q in range(n)])  # materialise a dense state

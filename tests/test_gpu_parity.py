@@ -128,6 +128,16 @@ def test_qft_closed_form(qs, n):
         assert maxdiff(psi, pins.qft_closed_form(n, x)) < TOL
 
 
+@pytest.mark.parametrize("name", sorted(W.ROSTER))
+def test_roster_gpu(qs, name):
+    """PAPER.md Table 2 roster (BV, HS, QAOA, QFT, QV, SC, VC) at 18 qubits
+    (specialised kernels) against the oracle."""
+    n = 18
+    gates = W.ROSTER[name](n)
+    psi, _ = sim_run(qs, n, gates)
+    assert maxdiff(psi, oracle.apply_circuit(n, gates)) < TOL
+
+
 @pytest.mark.parametrize("n", [3, 13, 22])
 def test_ghz(qs, n):
     psi, _ = sim_run(qs, n, W.ghz(n))

@@ -205,3 +205,26 @@ def test_invalid_gates_rejected():
         qs.plan_json(3, [W.Gate("UNITARY", (0,), (), (), bad)])
     with pytest.raises(qs.QSError):
         qs.plan_json(3, [W.Gate("DIAGONAL", (0,), (), (), np.array([1, 2]))])
+
+
+@pytest.mark.parametrize("name", sorted(W.ROSTER))
+@pytest.mark.parametrize("flags", [qs.QS_OPT_ALL, qs.QS_OPT_FUSE, 0])
+def test_roster_replay(name, flags):
+    """PAPER.md Table 2 roster circuits (L799-805) under the ablation modes:
+    plan replay equals the oracle."""
+    n = 12
+    gates = W.ROSTER[name](n)
+    plan = qs.plan_json(n, gates, config=qs.make_config(flags=flags), detail=True)
+    psi = replay(plan, n, 1)
+    assert np.max(np.abs(psi - oracle.apply_circuit(n, gates))) < 1e-11
+
+
+def test_nofusion_nonblocking_is_one_gate_per_pass():
+    """Without blocking or fusion every dense gate costs one state sweep; with
+    fusion only, gates whose targets fuse into <= F qubits share one."""
+    n = 14
+    gates = [W.Gate("RX", (q,), (), (0.1 * q,)) for q in range(n)]
+    p0 = qs.plan_json(n, gates, config=qs.make_config(flags=0), detail=True)
+    pf = qs.plan_json(n, gates, config=qs.make_config(flags=qs.QS_OPT_FUSE, fuse_cap=4), detail=True)
+    assert p0["stats"]["n_passes"] == n
+    assert pf["stats"]["n_passes"] == -(-n // 4)

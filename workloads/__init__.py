@@ -15,6 +15,9 @@ Constructions:
   diag_chain     diagonal-heavy RZ/CZ/CP chains with one RX barrier per layer.
   qaoa_maxcut    MaxCut QAOA on a seeded random d-regular graph.
   supremacy      Google-2019-like random circuit on a rows x cols grid.
+  bernstein_vazirani, hidden_shift, quantum_volume, variational,
+  supremacy_n    PAPER.md Table 2 roster (BV, HS, QV, VC, SC; L777-806).
+  qaoa_complete  PAPER.md Table 3 "5-level fully connected" QAOA (L715).
   random_circuit seeded mix of every supported kind (parity tests).
   fixture_f4     PAPER.md Fig. 4 (L652-682), reconstructed.
   fixture_f23    PAPER.md Fig. 2/3 (L336, L468-474), reconstructed (F23).
@@ -31,7 +34,8 @@ __all__ = [
     "Gate", "qft", "ghz", "rzz_full", "diag_chain", "qaoa_maxcut",
     "random_regular_graph", "supremacy", "random_circuit", "fixture_f4",
     "fixture_f23", "haar_unitary", "random_phases", "KIND_ARITY",
-    "DIAGONAL_KINDS", "splitmix64",
+    "DIAGONAL_KINDS", "splitmix64", "bernstein_vazirani", "hidden_shift",
+    "quantum_volume", "variational", "supremacy_n", "qaoa_complete", "ROSTER",
 ]
 
 # Number of targets per kind (None: taken from the matrix).
@@ -217,6 +221,92 @@ def supremacy(rows: int = 5, cols: int = 7, depth: int = 20, seed: int = 1,
                 g.append(Gate("CZ", (b,), (a,)))
     one_qubit_layer()
     return g
+
+
+# --------------------------------------------------------------------------
+# PAPER.md Table 2 roster (L777-806; "benchmark circuits drawn from various
+# application domains", cited to the qibojit benchmark suite).  The paper
+# gives names only; the constructions below are the textbook circuits in the
+# shape that suite uses (reading r6).
+# --------------------------------------------------------------------------
+
+def bernstein_vazirani(n: int, seed: int = 1) -> List[Gate]:
+    """BV: n-1 data qubits + ancilla n-1.  X(anc), H on all, CX(i -> anc)
+    for every set bit of a seeded secret, H on the data qubits."""
+    rng = np.random.default_rng(seed)
+    secret = [int(b) for b in rng.integers(0, 2, size=n - 1)]
+    anc = n - 1
+    g: List[Gate] = [Gate("X", (anc,))] + [Gate("H", (q,)) for q in range(n)]
+    g += [Gate("CX", (anc,), (i,)) for i in range(n - 1) if secret[i]]
+    g += [Gate("H", (q,)) for q in range(n - 1)]
+    return g
+
+
+def hidden_shift(n: int, seed: int = 1) -> List[Gate]:
+    """HS (bent-function hidden shift, n even): H all; X on the shift's set
+    bits; CZ(2i, 2i+1); X on the shift; H all; CZ(2i, 2i+1); H all."""
+    assert n % 2 == 0, "hidden shift needs an even qubit count"
+    rng = np.random.default_rng(seed)
+    shift = [int(b) for b in rng.integers(0, 2, size=n)]
+    H = [Gate("H", (q,)) for q in range(n)]
+    X = [Gate("X", (q,)) for q in range(n) if shift[q]]
+    CZ = [Gate("CZ", (2 * i + 1,), (2 * i,)) for i in range(n // 2)]
+    return H + X + CZ + X + H + list(CZ) + H
+
+
+def quantum_volume(n: int, depth: Optional[int] = None, seed: int = 1) -> List[Gate]:
+    """QV: `depth` (default n) layers; each pairs the qubits of a seeded
+    random permutation and applies a Haar-random 4x4 unitary per pair."""
+    rng = np.random.default_rng(seed)
+    g: List[Gate] = []
+    for _ in range(depth if depth is not None else n):
+        perm = [int(q) for q in rng.permutation(n)]
+        for i in range(0, n - 1, 2):
+            a, b = perm[i], perm[i + 1]
+            g.append(Gate("UNITARY", (a, b), (), (), haar_unitary(4, rng)))
+    return g
+
+
+def variational(n: int, layers: int = 5, seed: int = 1) -> List[Gate]:
+    """VC (hardware-efficient ansatz): per layer RY(theta) on every qubit,
+    CZ on the even pairs (0,1),(2,3)..., RY on every qubit, CZ on the odd
+    pairs (1,2),(3,4)...; a final RY layer.  theta ~ U[0, 2 pi)."""
+    rng = np.random.default_rng(seed)
+    ry = lambda: [Gate("RY", (q,), (), (float(rng.uniform(0, 2 * math.pi)),)) for q in range(n)]
+    g: List[Gate] = []
+    for _ in range(layers):
+        g += ry() + [Gate("CZ", (q + 1,), (q,)) for q in range(0, n - 1, 2)]
+        g += ry() + [Gate("CZ", (q + 1,), (q,)) for q in range(1, n - 1, 2)]
+    return g + ry()
+
+
+def supremacy_n(n: int, depth: int = 20, seed: int = 1) -> List[Gate]:
+    """SC on n qubits: the `supremacy` construction on the smallest grid of
+    width ceil(sqrt(n)) holding n qubits, couplers to absent sites dropped."""
+    cols = int(math.ceil(math.sqrt(n)))
+    rows = (n + cols - 1) // cols
+    full = supremacy(rows, cols, depth, seed)
+    return [x for x in full if max(x.support) < n]
+
+
+def qaoa_complete(n: int, p: int = 5, seed: int = 1) -> List[Gate]:
+    """PAPER.md L715/L811-858 Table 3 workload: "5-level fully connected"
+    QAOA -- H^n, then per level RZZ(gamma) on every pair j<k and RX(2 beta)
+    on every qubit."""
+    rng = np.random.default_rng(seed + 104729)
+    g: List[Gate] = [Gate("H", (q,)) for q in range(n)]
+    for _ in range(p):
+        gamma = float(rng.uniform(0, math.pi))
+        beta = float(rng.uniform(0, math.pi / 2))
+        g += [Gate("RZZ", (a, b), (), (gamma,)) for a in range(n) for b in range(a + 1, n)]
+        g += [Gate("RX", (q,), (), (2 * beta,)) for q in range(n)]
+    return g
+
+
+ROSTER = {
+    "bv": bernstein_vazirani, "hs": hidden_shift, "qaoa": lambda n: qaoa_maxcut(n, 4, 1, 3 if n % 2 == 0 else 4),
+    "qft": qft, "qv": quantum_volume, "sc": supremacy_n, "vc": variational,
+}
 
 
 # --------------------------------------------------------------------------
