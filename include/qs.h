@@ -112,6 +112,8 @@ typedef struct {
   double t_plan_ms;          /* host optimiser time of the last call          */
   double t_device_ms;        /* device time of the last call (CUDA events)    */
   double t_swap_ms;          /* part of t_device_ms spent in swaps            */
+  uint64_t n_fused_swaps;    /* swaps done by the preceding pass's peer stores
+                                 in the last call             */
 } qs_stats_t;
 
 typedef struct qs_ctx qs_ctx;

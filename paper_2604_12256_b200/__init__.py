@@ -67,7 +67,7 @@ class qs_stats_t(ctypes.Structure):
         "n_small_passes", "n_expand", "n_swaps", "n_substate_gates", "n_fused_diag",
         "bytes_hbm", "bytes_nvlink", "paper_updates", "naive_updates")] + [
         ("t_plan_ms", ctypes.c_double), ("t_device_ms", ctypes.c_double),
-        ("t_swap_ms", ctypes.c_double)]
+        ("t_swap_ms", ctypes.c_double), ("n_fused_swaps", ctypes.c_uint64)]
 
 
 _lib = None
@@ -134,29 +134,41 @@ def jit_info(sim=None) -> dict:
     return json.loads(buf.value.decode())
 
 
+_GATE_DTYPE = np.dtype({
+    "names": ["kind", "n_targets", "targets", "n_controls", "controls", "params", "matrix"],
+    "formats": [np.int32, np.int32, (np.int32, MAX_TARGETS), np.int32, (np.int32, MAX_CONTROLS),
+                (np.float64, 3), np.uint64],
+    "offsets": [getattr(qs_gate_t, f).offset for f in
+                ("kind", "n_targets", "targets", "n_controls", "controls", "params", "matrix")],
+    "itemsize": ctypes.sizeof(qs_gate_t),
+})
+
+
 def marshal_gates(gates: Sequence) -> tuple:
-    """Gate objects -> (qs_gate_t array, keep-alive list)."""
-    arr = (qs_gate_t * max(1, len(gates)))()
+    """Gate objects -> (qs_gate_t array, keep-alive list): filled column-wise
+    through a numpy view of the records (argument marshalling only)."""
+    n = len(gates)
+    arr = (qs_gate_t * max(1, n))()
     keep = []
+    if not n:
+        return arr, keep
+    v = np.frombuffer(arr, dtype=_GATE_DTYPE)
+    nt = [len(g.targets) for g in gates]
+    nc = [len(g.controls) for g in gates]
+    if max(nt) > MAX_TARGETS or max(nc) > MAX_CONTROLS:
+        raise ValueError("too many targets/controls")
+    v["kind"] = [KINDS[g.kind] for g in gates]
+    v["n_targets"] = nt
+    v["n_controls"] = nc
+    zt, zc, zp = (0,) * MAX_TARGETS, (0,) * MAX_CONTROLS, (0.0, 0.0, 0.0)
+    v["targets"] = [(tuple(g.targets) + zt)[:MAX_TARGETS] for g in gates]
+    v["controls"] = [(tuple(g.controls) + zc)[:MAX_CONTROLS] for g in gates]
+    v["params"] = [(tuple(g.params) + zp)[:3] for g in gates]
     for i, g in enumerate(gates):
-        r = arr[i]
-        r.kind = KINDS[g.kind]
-        r.n_targets = len(g.targets)
-        r.n_controls = len(g.controls)
-        if r.n_targets > MAX_TARGETS or r.n_controls > MAX_CONTROLS:
-            raise ValueError("too many targets/controls")
-        for j, q in enumerate(g.targets):
-            r.targets[j] = q
-        for j, q in enumerate(g.controls):
-            r.controls[j] = q
-        for j, p in enumerate(tuple(g.params)[:3]):
-            r.params[j] = p
         if getattr(g, "matrix", None) is not None:
             m = np.ascontiguousarray(np.asarray(g.matrix, dtype=np.complex128))
             keep.append(m)
-            r.matrix = m.ctypes.data
-        else:
-            r.matrix = None
+            v["matrix"][i] = m.ctypes.data
     return arr, keep
 
 
@@ -249,17 +261,29 @@ class Simulator:
         arr, keep = marshalled if marshalled is not None else marshal_gates(gates)
         self._check(self.lib.qs_apply_circuit(self.h, arr, len(gates)))
 
-    def state(self, offset: int = 0, count: Optional[int] = None) -> np.ndarray:
+    @staticmethod
+    def _out(out, count, dtype):
+        if out is None:
+            return np.empty(count, dtype=dtype)
+        if out.dtype != dtype or out.size < count or not out.flags.c_contiguous:
+            raise ValueError(f"out must be a C-contiguous {np.dtype(dtype).name} array of >= {count} elements")
+        return out
+
+    def state(self, offset: int = 0, count: Optional[int] = None,
+              out: Optional[np.ndarray] = None) -> np.ndarray:
+        """Amplitudes [offset, offset+count) in logical order.  `out` (e.g. a
+        view of pinned host memory) is filled in place and returned."""
         if count is None:
             count = (1 << self.n) - offset
-        out = np.empty(count, dtype=np.complex128)
+        out = self._out(out, count, np.complex128)
         self._check(self.lib.qs_get_state(self.h, out.ctypes.data, offset, count))
         return out
 
-    def probabilities(self, offset: int = 0, count: Optional[int] = None) -> np.ndarray:
+    def probabilities(self, offset: int = 0, count: Optional[int] = None,
+                      out: Optional[np.ndarray] = None) -> np.ndarray:
         if count is None:
             count = (1 << self.n) - offset
-        out = np.empty(count, dtype=np.float64)
+        out = self._out(out, count, np.float64)
         self._check(self.lib.qs_probabilities(self.h, out.ctypes.data, offset, count))
         return out
 

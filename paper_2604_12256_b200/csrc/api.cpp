@@ -40,8 +40,8 @@ cudaError_t launch_gather(const double2* state, double2* out, u64 off, u64 count
 bool jit_prepare(const unsigned char* blob, int device, void** fn_out, int* grid_per_sm,
                  size_t* smem_out, std::string& err, bool compile_only);
 cudaError_t jit_launch(void* fn, int grid, size_t smem, const unsigned char* dblob,
-                       double2* state, u64 rank_base, const u64* vtab, const void* pool_host,
-                       size_t pool_bytes, cudaStream_t st);
+                       double2* state, u64 rank_base, const u64* vtab, const u64* xpeer8,
+                       const void* pool_host, size_t pool_bytes, cudaStream_t st);
 int jit_table_cols(const unsigned char* blob, TabCols* v);
 cudaError_t launch_shape_table(const unsigned char* dblob, u64* tab, u64 rank_base, u64 n_chunks,
                                const TabCols& v, cudaStream_t st);
@@ -101,6 +101,9 @@ struct Shard {
   int8_t* dmap = nullptr;            // logical->physical map (device)
   u64* vtab = nullptr;               // per-chunk shape sums of the running pass
   size_t vtab_cap = 0;               // entries
+  double2* alloc[2] = {nullptr, nullptr};  // the two shard allocations (state,
+                                           // scratch at creation; they alternate)
+  double* bar = nullptr;             // rank mode: 1-element all-reduce = barrier
   std::vector<Timed> timed;          // per-launch events of the last call
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
@@ -128,6 +131,14 @@ struct qs_ctx {
   bool timing = true;
   uint64_t jit_launches = 0, jit_errors = 0;
   std::string jit_last_error;
+  // fused swaps: pointer swaps so far (all shards and ranks
+  // in lockstep), peer access state (0 unknown, 1 ready, -1 unavailable),
+  // rank mode: the peers' two allocations mapped through CUDA IPC
+  uint64_t swap_parity = 0;
+  int peers = 0;
+  std::vector<double2*> ipc;
+  bool fused_pending = false;
+  uint64_t n_fused_swaps = 0;
   // per kernel kind: launches, ms, algorithmic bytes (last call, shard 0..)
   uint64_t k_count[KK_NUM];
   double k_ms[KK_NUM];
@@ -191,6 +202,12 @@ int alloc_shard_memory(qs_ctx* ctx, Shard& s) {
   if (ctx->n_ranks > 1 && cudaMalloc(&s.scratch, bytes) != cudaSuccess)
     return set_err(ctx, QS_ENOMEM, "cudaMalloc swap buffer failed (" + std::to_string(bytes) + " B)");
   CU(cudaMalloc(&s.dmap, 64));
+  s.alloc[0] = s.state;
+  s.alloc[1] = s.scratch;
+  if (ctx->n_ranks > 1) {
+    CU(cudaMalloc(&s.bar, 64));
+    CU(cudaMemset(s.bar, 0, 64));
+  }
   CU(cudaEventCreate(&s.t0));
   CU(cudaEventCreate(&s.t1));
   return QS_OK;
@@ -228,6 +245,106 @@ int ensure_host_stage(qs_ctx* ctx, size_t bytes) {
   CU(cudaMallocHost(&ctx->host_stage, cap));
   ctx->host_stage_cap = cap;
   return QS_OK;
+}
+
+// ------------------------------------------------------------ fused swap
+// a pass right before a swap stores the pieces it exports
+// straight into the receive buffers of their destination ranks (NVLink peer
+// stores), so the exchange overlaps the pass instead of following it.  Needs
+// every receive buffer addressable: same device (loopback), peer access
+// (one process, several GPUs), or CUDA IPC mappings (one process per GPU;
+// handles exchanged once over the NCCL communicator).
+int ensure_peers(qs_ctx* ctx) {
+  if (ctx->peers) return ctx->peers;
+  ctx->peers = -1;
+  if (getenv("QS_NO_FUSED_SWAP") || ctx->n_ranks < 2) return ctx->peers;
+  if (ctx->mode == M_LOOPBACK) {
+    ctx->peers = 1;
+  } else if (ctx->mode == M_SINGLE) {
+    for (Shard& a : ctx->shards)
+      for (Shard& b : ctx->shards) {
+        if (a.device == b.device) continue;
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, a.device, b.device);
+        if (!can) return ctx->peers;
+        cudaSetDevice(a.device);
+        cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else if (e != cudaSuccess) return ctx->peers;
+      }
+    ctx->peers = 1;
+  } else {
+    // every rank takes part in both collectives (handle all-gather, then a
+    // min-vote on success) so that all of them make the same decision
+    Shard& sh = ctx->shards[0];
+    cudaSetDevice(sh.device);
+    cudaIpcMemHandle_t h[2];
+    memset(h, 0, sizeof h);
+    bool ok = cudaIpcGetMemHandle(&h[0], sh.alloc[0]) == cudaSuccess &&
+              cudaIpcGetMemHandle(&h[1], sh.alloc[1]) == cudaSuccess;
+    if (!ok) cudaGetLastError();
+    const size_t hb = sizeof h;
+    unsigned char* d = nullptr;
+    if (cudaMalloc(&d, hb * ctx->n_ranks + 16) != cudaSuccess) return ctx->peers;
+    std::vector<unsigned char> all(hb * ctx->n_ranks);
+    bool coll = cudaMemcpyAsync(d + hb * sh.rank, h, hb, cudaMemcpyHostToDevice, sh.stream) == cudaSuccess &&
+                ncclAllGather(d + hb * sh.rank, d, hb, ncclUint8, sh.comm, sh.stream) == ncclSuccess &&
+                cudaMemcpyAsync(all.data(), d, all.size(), cudaMemcpyDeviceToHost, sh.stream) == cudaSuccess &&
+                cudaStreamSynchronize(sh.stream) == cudaSuccess;
+    ok = ok && coll;
+    std::vector<double2*> mapped(2 * ctx->n_ranks, nullptr);
+    for (int r = 0; r < ctx->n_ranks && ok; r++) {
+      if (r == sh.rank) {
+        mapped[2 * r] = sh.alloc[0];
+        mapped[2 * r + 1] = sh.alloc[1];
+        continue;
+      }
+      for (int k = 0; k < 2 && ok; k++) {
+        cudaIpcMemHandle_t hk;
+        memcpy(&hk, all.data() + hb * r + sizeof(cudaIpcMemHandle_t) * k, sizeof hk);
+        void* p = nullptr;
+        if (cudaIpcOpenMemHandle(&p, hk, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+          cudaGetLastError();
+          ok = false;
+        } else {
+          mapped[2 * r + k] = (double2*)p;
+        }
+      }
+    }
+    double vote = ok ? 1.0 : 0.0;
+    double* dv = reinterpret_cast<double*>(d + hb * ctx->n_ranks);
+    coll = coll && cudaMemcpyAsync(dv, &vote, sizeof vote, cudaMemcpyHostToDevice, sh.stream) == cudaSuccess &&
+           ncclAllReduce(dv, dv, 1, ncclDouble, ncclMin, sh.comm, sh.stream) == ncclSuccess &&
+           cudaMemcpyAsync(&vote, dv, sizeof vote, cudaMemcpyDeviceToHost, sh.stream) == cudaSuccess &&
+           cudaStreamSynchronize(sh.stream) == cudaSuccess;
+    cudaFree(d);
+    ctx->ipc = mapped;  // closed at destroy (whatever was opened)
+    if (coll && vote == 1.0) ctx->peers = 1;
+  }
+  return ctx->peers;
+}
+
+// Receive buffer of rank d right now (the two allocations alternate with
+// every pointer swap, in lockstep on all ranks).
+double2* recv_buffer(qs_ctx* ctx, int d) {
+  if (ctx->mode != M_RANK) return ctx->shards[d].scratch;
+  return ctx->ipc[2 * d + ((ctx->swap_parity & 1) ? 0 : 1)];
+}
+
+// Destination bases of rank r's exported pieces for the swap `st`: piece s
+// of rank r lands in the receive buffer of rank dest(r, s) at piece u(r), so
+// the base is that buffer + (u(r) - s) * 2^(nl-j) amplitudes.
+void fused_targets(qs_ctx* ctx, const Step& st, int r, u64 out[8]) {
+  const int j = st.j, nl = ctx->nl;
+  int ur = 0, d0 = r;
+  for (int i = 0; i < j; i++) ur |= ((r >> (st.gpos[i] - nl)) & 1) << i;
+  for (int s = 0; s < 8; s++) {
+    out[s] = 0;
+    if (s >= (1 << j)) continue;
+    int d = d0;
+    for (int i = 0; i < j; i++) d = (d & ~(1 << (st.gpos[i] - nl))) | (((s >> i) & 1) << (st.gpos[i] - nl));
+    out[s] = (u64)recv_buffer(ctx, d) + (((u64)ur << (nl - j)) - ((u64)s << (nl - j))) * sizeof(double2);
+  }
 }
 
 // ----------------------------------------------------------------- swap
@@ -371,8 +488,35 @@ int execute(qs_ctx* ctx, const Plan& plan) {
         b = get_event(s0);
         CU(cudaEventRecord(a, s0.stream));
       }
-      rc = exec_swap(ctx, st);
-      if (rc) return rc;
+      if (st.fusable && ctx->fused_pending) {
+        // the preceding pass already stored every piece in its destination's
+        // receive buffer: wait for all of them, then the buffers trade roles
+        if (ctx->mode == M_RANK) {
+          for (Shard& sh : ctx->shards) {
+            CU(cudaSetDevice(sh.device));
+            NC(ncclAllReduce(sh.bar, sh.bar, 1, ncclDouble, ncclSum, sh.comm, sh.stream));
+          }
+        } else {
+          std::vector<cudaEvent_t> done;
+          for (Shard& sh : ctx->shards) {
+            CU(cudaSetDevice(sh.device));
+            done.push_back(get_event(sh));
+            CU(cudaEventRecord(done.back(), sh.stream));
+          }
+          for (size_t t = 0; t < ctx->shards.size(); t++) {
+            CU(cudaSetDevice(ctx->shards[t].device));
+            for (size_t u = 0; u < done.size(); u++)
+              if (u != t) CU(cudaStreamWaitEvent(ctx->shards[t].stream, done[u], 0));
+          }
+        }
+        for (Shard& sh : ctx->shards) std::swap(sh.state, sh.scratch);
+        ctx->n_fused_swaps++;
+      } else {
+        rc = exec_swap(ctx, st);
+        if (rc) return rc;
+      }
+      ctx->fused_pending = false;
+      ctx->swap_parity++;
       if (ctx->timing) {
         CU(cudaSetDevice(s0.device));
         CU(cudaEventRecord(b, s0.stream));
@@ -428,6 +572,7 @@ int execute(qs_ctx* ctx, const Plan& plan) {
           CU(launch_permute(sh.state, sh.scratch, shard_amps, st.gpos.data(), st.lpos.data(),
                             (int)st.gpos.size(), sh.stream));
           std::swap(sh.state, sh.scratch);
+          if (si == 0) ctx->swap_parity++;
           ctx->launches++;
           kind = KK_SWAP;
           bytes = 32ull << ctx->nl;
@@ -458,6 +603,22 @@ int execute(qs_ctx* ctx, const Plan& plan) {
           int per_sm = 1;
           size_t smem = 0;
           std::string jerr;
+          // fused swap: this pass exports the next swap's pieces (decided the
+          // same way on every shard and rank: the plan + collective peer setup)
+          u64 xp[8];
+          for (int s = 0; s < 8; s++) xp[s] = (u64)buf;
+          bool fuse = false;
+          if (h.x_mask && k + 1 < plan.steps.size()) {
+            const Step& nx = plan.steps[k + 1];
+            if (nx.type == Step::SWAP && nx.fusable) {
+              if (ensure_peers(ctx) == 1) {
+                fused_targets(ctx, nx, sh.rank, xp);
+                fuse = true;
+                ctx->fused_pending = true;
+              }
+              CU(cudaSetDevice(sh.device));
+            }
+          }
           if (p.kernel != KK_SMALL && p.nl >= ctx->cfg.jit_min_qubits &&
               jit_prepare(blobs[si].data() + blob_off[si][k], sh.device, &fn, &per_sm, &smem, jerr,
                           false)) {
@@ -478,12 +639,19 @@ int execute(qs_ctx* ctx, const Plan& plan) {
               CU(launch_shape_table(dblob, sh.vtab, h.rank_base, h.n_chunks, vl, sh.stream));
               ctx->launches++;
             }
-            CU(jit_launch(fn, (int)grid, smem, dblob, buf, h.rank_base, sh.vtab, hb + h.off_pool, pb,
-                          sh.stream));
+            CU(jit_launch(fn, (int)grid, smem, dblob, buf, h.rank_base, sh.vtab, xp, hb + h.off_pool,
+                          pb, sh.stream));
             ctx->jit_launches++;
           } else {
             if (!jerr.empty()) ctx->jit_errors++, ctx->jit_last_error = jerr;
             CU(launch_pass(p.kernel, dblob, h, buf, sh.stream));
+            if (fuse) {
+              // interpreter kernels store locally: export the pieces by copies
+              const size_t piece = (size_t)1 << h.x_shift;
+              for (int s = 0; s <= h.x_mask; s++)
+                CU(cudaMemcpyAsync((double2*)xp[s] + (size_t)s * piece, buf + (size_t)s * piece,
+                                   piece * sizeof(double2), cudaMemcpyDefault, sh.stream));
+            }
           }
           ctx->launches++;
           kind = (p.buf == 0) ? p.kernel : KK_SUB;  // full-state passes only per kernel
@@ -532,6 +700,7 @@ int execute(qs_ctx* ctx, const Plan& plan) {
     }
   }
   ctx->stats.t_swap_ms = tswap;
+  ctx->stats.n_fused_swaps = ctx->n_fused_swaps;
   return QS_OK;
 }
 
@@ -667,6 +836,13 @@ void qs_destroy(qs_ctx* ctx) {
     cudaSetDevice(s.device);
     if (s.stream) cudaStreamSynchronize(s.stream);
   }
+  if (ctx->mode == M_RANK && !ctx->ipc.empty()) {
+    cudaSetDevice(ctx->shards[0].device);
+    for (int r = 0; r < ctx->n_ranks; r++)
+      if (r != ctx->shards[0].rank)
+        for (int k = 0; k < 2; k++)
+          if (ctx->ipc[2 * r + k]) cudaIpcCloseMemHandle(ctx->ipc[2 * r + k]);
+  }
   for (Shard& s : ctx->shards) {
     cudaSetDevice(s.device);
     if (s.comm) ncclCommDestroy(s.comm);
@@ -677,6 +853,7 @@ void qs_destroy(qs_ctx* ctx) {
     cudaFree(s.tmp);
     cudaFree(s.dmap);
     cudaFree(s.vtab);
+    cudaFree(s.bar);
     for (cudaEvent_t e : s.ev_pool) cudaEventDestroy(e);
     if (s.t0) cudaEventDestroy(s.t0);
     if (s.t1) cudaEventDestroy(s.t1);
@@ -788,20 +965,24 @@ static int readout(qs_ctx* ctx, double* host_out, uint64_t offset, uint64_t coun
     }
     CU(cudaMemcpyAsync(sh.dmap, hmap, 64, cudaMemcpyHostToDevice, sh.stream));
   }
-  memset(host_out, 0, count * per * sizeof(double));
+  // One shard per process (rank mode, or a single GPU): the slice goes
+  // straight into the caller's buffer (a DMA when the buffer is pinned).
+  // Several shards in this process: each gathers its part (zeros elsewhere)
+  // and the host sums them.
+  const bool direct = ctx->mode == M_RANK || ctx->shards.size() == 1;
+  if (!direct) memset(host_out, 0, count * per * sizeof(double));
   for (uint64_t done = 0; done < count; done += slice) {
     const uint64_t c = std::min(slice, count - done);
-    if (ctx->mode == M_RANK) {
+    if (direct) {
       Shard& sh = ctx->shards[0];
       CU(cudaSetDevice(sh.device));
       CU(launch_gather(sh.state, sh.tmp, offset + done, c, ctx->n, sh.dmap, ctx->nl,
                        (u64)sh.rank, probs, sh.stream));
-      if (ctx->n_ranks > 1)
+      if (ctx->mode == M_RANK && ctx->n_ranks > 1)
         NC(ncclAllReduce(sh.tmp, sh.tmp, c * per, ncclDouble, ncclSum, sh.comm, sh.stream));
-      CU(cudaMemcpyAsync(ctx->host_tmp, sh.tmp, c * per * sizeof(double), cudaMemcpyDeviceToHost,
-                         sh.stream));
+      CU(cudaMemcpyAsync(host_out + done * per, sh.tmp, c * per * sizeof(double),
+                         cudaMemcpyDeviceToHost, sh.stream));
       CU(cudaStreamSynchronize(sh.stream));
-      memcpy(host_out + done * per, ctx->host_tmp, c * per * sizeof(double));
     } else {
       for (Shard& sh : ctx->shards) {
         CU(cudaSetDevice(sh.device));

@@ -810,10 +810,13 @@ struct Gen {
     const size_t npool = (h.total_bytes - h.off_pool) / sizeof(double);
     param_pool = npool > 0 && npool <= kMaxParamPool;
     if (param_pool) o << "struct QsPool { double v[" << npool << "]; };\n";
+    // fused swap: destination base per value of the exported
+    // top local bits (receive buffers of this rank or its peers, by value)
+    o << "struct QsXPeer { u64 v[8]; };\n";
     o << "extern \"C\" __global__ void __launch_bounds__(" << nthreads << ", " << (NG == 1 && NB <= 1 ? 2 : 1)
       << ")\n" << kname
       << "(const unsigned char* __restrict__ blob, double2* __restrict__ state, u64 rank_base, "
-         "const u64* __restrict__ vtab"
+         "const u64* __restrict__ vtab, const QsXPeer xp"
       << (param_pool ? ", const QsPool P" : "") << ") {\n";
     o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n";
     const size_t buf_bytes = (size_t)NB * CH * 16;
@@ -1036,12 +1039,19 @@ struct Gen {
         o << "    " << A(r) << " = make_double2(" << A(r) << ".x * " << hex(h.scale) << ", " << A(r)
           << ".y * " << hex(h.scale) << ");\n";
     }
-    o << "    { double2* __restrict__ so = state + (cb | tpo);\n";
+    if (h.x_mask)  // the exported top bits are chunk-index bits: one destination per chunk
+      o << "    { double2* __restrict__ so = reinterpret_cast<double2*>(xp.v[(cb >> " << h.x_shift << ") & "
+        << h.x_mask << "u]) + (cb | tpo);\n";
+    else
+      o << "    { double2* __restrict__ so = state + (cb | tpo);\n";
     for (int r = 0; r < kNReg; r++)
       o << "      so[" << u(reg_phys(nlay - 1, r, true)) << "] = " << A(r) << ";\n";
     o << "    }\n";
     if (use_vtab) o << "    if (tid < " << NV << "u) scnx[tmap[tid]] = nxv;\n    gbar(1u + grp);\n";
-    o << "  }\n}\n";
+    o << "  }\n";
+    // peer stores must be performed before the barrier that publishes them
+    if (h.x_mask) o << "  __threadfence_system();\n";
+    o << "}\n";
     std::string s = o.str();
     if (n_hoist) s.insert(loop_pos, "  if (grp == 0) {\n" + pre.str() + "  }\n  __syncthreads();\n");
     if (n_table)
@@ -1283,8 +1293,8 @@ int jit_table_cols(const unsigned char* blob, TabCols* v) {
 }
 
 cudaError_t jit_launch(void* fn, int grid, size_t smem, const unsigned char* dblob,
-                       double2* state, u64 rank_base, const u64* vtab, const void* pool_host,
-                       size_t pool_bytes, cudaStream_t st) {
+                       double2* state, u64 rank_base, const u64* vtab, const u64* xpeer8,
+                       const void* pool_host, size_t pool_bytes, cudaStream_t st) {
   Driver& d = driver();
   int threads = kThreads;
   {
@@ -1292,8 +1302,11 @@ cudaError_t jit_launch(void* fn, int grid, size_t smem, const unsigned char* dbl
     auto it = g_threads.find(fn);
     if (it != g_threads.end()) threads = it->second;
   }
-  void* args[] = {(void*)&dblob, (void*)&state, (void*)&rank_base, (void*)&vtab, (void*)pool_host};
-  if (!pool_bytes) args[4] = nullptr;
+  u64 xp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (xpeer8) memcpy(xp, xpeer8, sizeof xp);
+  void* args[] = {(void*)&dblob, (void*)&state, (void*)&rank_base, (void*)&vtab, (void*)xp,
+                  (void*)pool_host};
+  if (!pool_bytes) args[5] = nullptr;
   CUresult r = d.launch((CUfunction)fn, (unsigned)grid, 1, 1, (unsigned)threads, 1, 1, (unsigned)smem,
                         (CUstream)st, args, nullptr);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorLaunchFailure;

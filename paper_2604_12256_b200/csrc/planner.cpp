@@ -659,6 +659,21 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
     st.j = j;
     st.gpos = gpos;
     st.lpos = top;
+    // f1: the exchange can ride on the stores of the pass right before it
+    // (no permute or expand in between; a specialised kernel; its output
+    // positions clear of the exported top positions, which then come from
+    // the chunk index and select one destination per chunk)
+    if (buf == 0 && !plan.steps.empty() && plan.steps.back().type == Step::PASS) {
+      PassPlan& lp = plan.steps.back().pass;
+      bool ok = lp.buf == 0 && lp.kernel != KK_SMALL && lp.nl >= S.cfg->jit_min_qubits;
+      for (int p : lp.opos)
+        if (p >= nl - j) ok = false;
+      if (ok) {
+        lp.x_j = j;
+        st.fusable = true;
+        plan.stats.n_fusable_swaps++;
+      }
+    }
     // relabel: logical at gpos[i] <-> logical at lpos[i]
     for (int i = 0; i < j; i++) std::swap(map[inv[st.gpos[i]]], map[inv[st.lpos[i]]]);
     plan.steps.push_back(st);
@@ -853,6 +868,8 @@ int encode_pass(const PassPlan& p, int rank, std::vector<unsigned char>& out, st
     }
   }
   h.scale = 1.0;
+  h.x_shift = p.x_j ? p.nl - p.x_j : 0;
+  h.x_mask = p.x_j ? (1 << p.x_j) - 1 : 0;
   int n_hu = 0;
   std::vector<KOp> kops;
   std::vector<KGroup> kgroups;
@@ -1192,7 +1209,7 @@ std::string plan_to_json(const Plan& plan, bool detail) {
   o << ",\"stats\":{\"n_gates_in\":" << s.n_gates_in << ",\"n_passes\":" << s.n_passes
     << ",\"n_chunk\":" << s.n_chunk << ",\"n_dense\":" << s.n_dense << ",\"n_diag\":" << s.n_diag
     << ",\"n_small\":" << s.n_small << ",\"n_expand\":" << s.n_expand
-    << ",\"n_swaps\":" << s.n_swaps << ",\"n_sub_gates\":" << s.n_sub_gates
+    << ",\"n_swaps\":" << s.n_swaps << ",\"n_fusable_swaps\":" << s.n_fusable_swaps << ",\"n_sub_gates\":" << s.n_sub_gates
     << ",\"n_fused_diag\":" << s.n_fused_diag << ",\"paper_updates\":" << s.paper_updates
     << ",\"naive_updates\":" << s.naive_updates << ",\"bytes_hbm\":" << s.bytes_hbm
     << ",\"bytes_nvlink\":" << s.bytes_nvlink << ",\"booster_rounds\":[";
@@ -1241,11 +1258,12 @@ std::string plan_to_json(const Plan& plan, bool detail) {
         o << "],\"lpos\":[";
         for (size_t k = 0; k < st.lpos.size(); k++) o << (k ? "," : "") << st.lpos[k];
         o << "]";
+        if (st.type == Step::SWAP) o << ",\"fusable\":" << (st.fusable ? "true" : "false");
         break;
       case Step::PASS: {
         const PassPlan& p = st.pass;
         o << "\"type\":\"pass\",\"kernel\":\"" << kname(p.kernel) << "\",\"buf\":" << p.buf
-          << ",\"nl\":" << p.nl << ",\"src_mode\":" << p.src_mode
+          << ",\"nl\":" << p.nl << ",\"src_mode\":" << p.src_mode << ",\"x_j\":" << p.x_j
           << ",\"cpos\":[";
         for (size_t k = 0; k < p.cpos.size(); k++) o << (k ? "," : "") << p.cpos[k];
         o << "],\"opos\":[";

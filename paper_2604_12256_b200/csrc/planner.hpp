@@ -56,6 +56,10 @@ struct PassPlan {
   int src_mode = 0;           // 0 load, 1 expand (booster), 2 basis state
   std::vector<int> exp_bufs, exp_lo, exp_len;
   uint64_t basis = 0;
+  // the following SWAP's exchange is fused into this pass's
+  // stores -- output indices whose top x_j local bits are s go straight to the
+  // receive buffer of the rank the swap sends piece s to (0: not fused)
+  int x_j = 0;
   // filled by encode_pass
   std::vector<std::vector<int>> phase_regs;  // per phase: chunk bits held in registers
   std::vector<int> op_phase;
@@ -70,6 +74,7 @@ struct Step {
   int j = 0;                  // SWAP: number of exchanged qubits
   std::vector<int> gpos;      // SWAP: global positions exchanged with
   std::vector<int> lpos;      //       local positions (top j)
+  bool fusable = false;       // SWAP: the preceding pass may do the exchange
   int src_a = 0, src_b = 0;   // SUB_MERGE: dst = A (low) (x) B (high)
   std::vector<int> exp_bufs;  // EXPAND (and fused expand): sub-state ids
   std::vector<int> exp_lo, exp_len;
@@ -84,7 +89,7 @@ struct PlanStats {
   uint64_t n_gates_in = 0, n_passes = 0, n_chunk = 0, n_dense = 0, n_diag = 0,
            n_small = 0, n_expand = 0, n_swaps = 0, n_sub_gates = 0,
            n_fused_diag = 0, paper_updates = 0, naive_updates = 0,
-           bytes_hbm = 0, bytes_nvlink = 0;
+           bytes_hbm = 0, bytes_nvlink = 0, n_fusable_swaps = 0;
   std::vector<std::vector<int>> booster_rounds;  // gate counts per round/group
 };
 

@@ -1,0 +1,12 @@
+# bench (default, with cpu baseline + e2e), launch list, full ncu of the QFT-30 passes
+cd $GRAFT_REPO_ROOT
+timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1
+echo "bench rc=$?" >> gpurun_out/bench_default.log
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0"
+$CMD > gpurun_out/plain.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
+CMD1="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 0"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:jit -s 2 -c 2 \
+  -o gpurun_out/prof_qft $CMD1 > gpurun_out/ncu.log 2>&1
+echo "ncu rc=$?" >> gpurun_out/ncu.log

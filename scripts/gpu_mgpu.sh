@@ -1,11 +1,14 @@
-# 2-GPU checks: rank-mode parity (NCCL swaps) + bench at N=2 (torchrun)
+# GPU tests + 2-GPU checks: rank-mode parity (NCCL / fused swaps) + benches at N=2 (torchrun)
 cd $GRAFT_REPO_ROOT
-nvidia-smi topo -m > gpurun_out/topo.txt 2>&1
+timeout 1200 python -m pytest tests -m gpu -q -x --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 \
   scripts/mgpu_check.py > gpurun_out/mgpu_check.log 2>&1
 echo "mgpu rc=$?" >> gpurun_out/mgpu_check.log
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 \
-  bench.py --gpus 2 --steps 3 --warmup 3 > gpurun_out/bench_n2.log 2>&1
+  bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_n2.log 2>&1
 echo "bench2 rc=$?" >> gpurun_out/bench_n2.log
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29513 \
   bench.py --gpus 2 --workload qaoa --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench_n2_qaoa.log 2>&1
+QS_NO_FUSED_SWAP=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29514 \
+  bench.py --gpus 2 --workload qaoa --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench_n2_qaoa_nofuse.log 2>&1

@@ -60,7 +60,7 @@ def main():
                 ok = err < 1e-12
                 bad += not ok
                 print(json.dumps({"case": name, "n": n, "world": world, "jit_min": jit, "max_abs_diff": err,
-                                  "swaps": st["n_swaps"], "passes": st["n_passes"], "ok": ok}), flush=True)
+                                  "swaps": st["n_swaps"], "fused_swaps": st["n_fused_swaps"], "passes": st["n_passes"], "ok": ok}), flush=True)
     # large: QFT closed form at 28 + log2(world) qubits, sampled
     n = 28 + int(math.log2(world))
     x = 123456789 % (1 << n)
@@ -79,7 +79,7 @@ def main():
         ok = worst < 1e-12
         bad += not ok
         print(json.dumps({"case": "qft%d_closed_form" % n, "world": world, "max_abs_diff": worst,
-                          "swaps": st["n_swaps"], "passes": st["n_passes"], "t_swap_ms": st["t_swap_ms"],
+                          "swaps": st["n_swaps"], "fused_swaps": st["n_fused_swaps"], "passes": st["n_passes"], "t_swap_ms": st["t_swap_ms"],
                           "t_device_ms": st["t_device_ms"], "ok": ok}), flush=True)
     # forced swaps: a circuit that touches the global qubits with dense gates
     n = 24
@@ -97,7 +97,7 @@ def main():
         err = float(np.max(np.abs(psi - want)))
         ok = err < 1e-12 and (world == 1 or st["n_swaps"] >= 1)
         bad += not ok
-        print(json.dumps({"case": "rx_layers24", "world": world, "max_abs_diff": err, "swaps": st["n_swaps"],
+        print(json.dumps({"case": "rx_layers24", "world": world, "max_abs_diff": err, "swaps": st["n_swaps"], "fused_swaps": st["n_fused_swaps"],
                           "bytes_nvlink": st["bytes_nvlink"], "t_swap_ms": st["t_swap_ms"], "ok": ok}),
               flush=True)
     dist.barrier()
@@ -114,7 +114,7 @@ def main():
         ok = err < 1e-12
         bad += not ok
         print(json.dumps({"case": "single_process_%dgpu" % world, "max_abs_diff": err,
-                          "swaps": st["n_swaps"], "ok": ok}), flush=True)
+                          "swaps": st["n_swaps"], "fused_swaps": st["n_fused_swaps"], "ok": ok}), flush=True)
     dist.barrier()
     dist.destroy_process_group()
     sys.exit(1 if bad else 0)

@@ -194,6 +194,22 @@ def test_loopback_sharded(qs, ranks, n):
     assert maxdiff(psi, oracle.apply_circuit(n, gates, x=3)) < TOL
 
 
+@pytest.mark.parametrize("ranks", [2, 4, 8])
+def test_loopback_fused_swaps(qs, ranks):
+    """SURVEY 8(f) f1 on one GPU: with specialised kernels everywhere the pass
+    before each fusable swap stores the exported pieces straight into the
+    other shards' receive buffers; parity with the oracle and the swaps are
+    reported as fused."""
+    n = 18
+    gates = W.qaoa_maxcut(n, 3, 2)
+    psi, st = sim_run(qs, n, gates, ranks=ranks, jit_min_qubits=0)
+    assert st["n_swaps"] >= 2 and st["n_fused_swaps"] >= 1
+    assert maxdiff(psi, oracle.apply_circuit(n, gates)) < TOL
+    psi2, st2 = sim_run(qs, n, W.random_circuit(n, 160, 5 + ranks, diag_bias=0.3), basis=3,
+                        ranks=ranks, jit_min_qubits=0)
+    assert maxdiff(psi2, oracle.apply_circuit(n, W.random_circuit(n, 160, 5 + ranks, diag_bias=0.3), x=3)) < TOL
+
+
 def test_loopback_qaoa_swaps(qs):
     n = 18
     gates = W.qaoa_maxcut(n, 3, 2)

@@ -228,3 +228,23 @@ def test_nofusion_nonblocking_is_one_gate_per_pass():
     pf = qs.plan_json(n, gates, config=qs.make_config(flags=qs.QS_OPT_FUSE, fuse_cap=4), detail=True)
     assert p0["stats"]["n_passes"] == n
     assert pf["stats"]["n_passes"] == -(-n // 4)
+
+
+def test_fusable_swaps_marked():
+    """a swap right after a specialised pass is marked fusable
+    and that pass exports the swap's j top local bits, which lie outside its
+    chunk (so they select one destination per chunk)."""
+    n, ranks = 18, 4
+    gates = W.qaoa_maxcut(n, 3, 2)
+    plan = qs.plan_json(n, gates, n_ranks=ranks, config=qs.make_config(jit_min_qubits=0), detail=True)
+    steps = plan["steps"]
+    fused = [i for i, s in enumerate(steps) if s["type"] == "swap" and s["fusable"]]
+    assert fused and plan["stats"]["n_fusable_swaps"] == len(fused)
+    nl = n - 2
+    for i in fused:
+        p = steps[i - 1]
+        assert p["type"] == "pass" and p["x_j"] == steps[i]["j"]
+        assert all(q < nl - p["x_j"] for q in p["opos"])
+    # replay (the fused exchange has the swap's semantics) still matches
+    psi = replay(plan, n, ranks)
+    assert np.max(np.abs(psi - oracle.apply_circuit(n, gates))) < 1e-11
