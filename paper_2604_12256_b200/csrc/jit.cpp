@@ -727,6 +727,21 @@ struct Gen {
       (v ? vary : cons).push_back(j);
     }
     o << kPrelude;
+    // Processing order of the chunks.  A pass that exports a swap's pieces
+    // (x_mask) rotates the chunk id so that its top bits -- the destination
+    // rank -- change fastest: the CTAs in flight write to every destination
+    // at once instead of all of them streaming into one peer at a time.
+    {
+      int B = 0;
+      while ((1ull << B) < h.n_chunks) B++;
+      int J = 0;
+      while ((1 << J) <= h.x_mask) J++;
+      if (h.x_mask && J <= B)
+        o << "__device__ __forceinline__ u64 corder(u64 c) { return (c >> " << J << ") | ((c & "
+          << h.x_mask << "ull) << " << B - J << "); }\n";
+      else
+        o << "__device__ __forceinline__ u64 corder(u64 c) { return c; }\n";
+    }
     auto emit_arr = [&](const char* name, const std::vector<int>& v) {
       o << "__device__ const int " << name << "[" << std::max<size_t>(1, v.size()) << "] = {";
       for (size_t i = 0; i < v.size(); i++) o << (i ? "," : "") << v[i];
@@ -858,6 +873,7 @@ struct Gen {
     o << "  const u64 tpo = " << tphys_expr(nlay - 1, true) << ";\n";
     const std::string N = u(h.n_chunks);
     auto chunk_of = [&](const std::string& k) { return "(blockIdx.x + (u64)(" + k + ") * gridDim.x)"; };
+
     if (pipe) {
       o << "  if (threadIdx.x == 0) {\n"
         << "    for (int b = 0; b < " << NB << "; b++) { mbar_init(mbar + b, " << (use_tma ? 1 : kThreads)
@@ -868,7 +884,7 @@ struct Gen {
     if (use_tma) {
       o << "  const int tcl0 = " << tc_expr(0) << ";\n";
       o << "  for (u32 k = grp; k < " << NB << "u; k += " << NG << "u)\n"
-        << "    if (tid < 32 && " << chunk_of("k") << " < " << N << ") { issue(state, " << chunk_of("k")
+        << "    if (tid < 32 && " << chunk_of("k") << " < " << N << ") { issue(state, corder(" << chunk_of("k") << ")"
         << ", bufs + k * " << CH << ", mbar + k, tid); if (tid == 0) issued[k] = 1u; }\n";
     } else if (pipe) {
       std::string tpd = "(0ull";
@@ -876,7 +892,7 @@ struct Gen {
         tpd += " | ((u64)((tid >> " + std::to_string(i) + ") & 1u) << " + std::to_string((int)h.cpos[i]) + ")";
       o << "  const u64 tpd = " << tpd << ");\n  const int sd = swz((int)tid);\n";
       o << "  for (u32 k = grp; k < " << NB << "u; k += " << NG << "u)\n"
-        << "    if (" << chunk_of("k") << " < " << N << ") { issue_async(state, " << chunk_of("k")
+        << "    if (" << chunk_of("k") << " < " << N << ") { issue_async(state, corder(" << chunk_of("k") << ")"
         << ", bufs + k * " << CH << ", mbar + k, tpd, sd); if (tid == 0) issued[k] = 1u; }\n";
     }
     // level 1, constant shapes: once
@@ -905,12 +921,13 @@ struct Gen {
     const std::string NV = std::to_string(W);
     if (use_vtab)
       o << "  { const u64 c0 = " << chunk_of("grp") << ";\n    if (tid < " << NV << "u && c0 < " << N
-        << ") scoef[tmap[tid]] = __ldg(vtab + c0 * " << NV << "ull + tid); }\n  __syncthreads();\n";
+        << ") scoef[tmap[tid]] = __ldg(vtab + corder(c0) * " << NV << "ull + tid); }\n  __syncthreads();\n";
     o << "  double2 a0, a1, a2, a3, a4, a5, a6, a7, a8, a9, a10, a11, a12, a13, a14, a15;\n";
     const size_t loop_pos = o.str().size();  // hoisted code goes here
     o << "  for (u32 k = grp;; k += " << NG << "u) {\n"
-      << "    const u64 chunk = " << chunk_of("k") << ";\n"
-      << "    if (chunk >= " << N << ") break;\n";
+      << "    const u64 craw = " << chunk_of("k") << ";\n"
+      << "    if (craw >= " << N << ") break;\n"
+      << "    const u64 chunk = corder(craw);\n";
     if (pipe) o << "    const u32 kb = k % " << NB << "u;\n    double2* const sch = bufs + kb * " << CH << ";\n";
     else if (xchg) o << "    double2* const sch = bufs + grp * " << CH << ";\n";
     const std::string nxt = chunk_of("k + " + std::to_string(NB));
@@ -919,9 +936,9 @@ struct Gen {
     const std::string refill =
         use_tma ? "    gbar(1u + grp);  // every thread is done reading the buffer\n"
                   "    if (tid < 32 && " + nxt + " < " + N +
-                  ") { fence_proxy_async(); issue(state, " + nxt + ", sch, mbar + kb, tid); " + count + " }\n"
+                  ") { fence_proxy_async(); issue(state, corder(" + nxt + "), sch, mbar + kb, tid); " + count + " }\n"
                 : "    gbar(1u + grp);  // every thread is done reading the buffer\n"
-                  "    if (" + nxt + " < " + N + ") { issue_async(state, " + nxt + ", sch, mbar + kb, tpd, sd); " +
+                  "    if (" + nxt + " < " + N + ") { issue_async(state, corder(" + nxt + "), sch, mbar + kb, tpd, sd); " +
                   count + " }\n";
     o << "    const u64 cb = " << cbexpr << ";\n";
     o << "    const u64 cphys = cb | rank_base;\n    (void)cphys;\n";
@@ -934,7 +951,7 @@ struct Gen {
         << "    (void)cisv;\n"
         << "    u64 nxv = 0ull;\n"
         << "    { const u64 nc = " << chunk_of("k + " + std::to_string(NG)) << ";\n"
-        << "      if (tid < " << NV << "u && nc < " << N << ") nxv = __ldg(vtab + nc * " << NV << "ull + tid); }\n";
+        << "      if (tid < " << NV << "u && nc < " << N << ") nxv = __ldg(vtab + corder(nc) * " << NV << "ull + tid); }\n";
     } else if (!vary.empty()) {
       o << "    gbar(1u + grp);\n";
       if (!vbig.empty()) level1("vmap", vbig.size(), true);
@@ -1039,14 +1056,22 @@ struct Gen {
         o << "    " << A(r) << " = make_double2(" << A(r) << ".x * " << hex(h.scale) << ", " << A(r)
           << ".y * " << hex(h.scale) << ");\n";
     }
-    if (h.x_mask)  // the exported top bits are chunk-index bits: one destination per chunk
-      o << "    { double2* __restrict__ so = reinterpret_cast<double2*>(xp.v[(cb >> " << h.x_shift << ") & "
-        << h.x_mask << "u]) + (cb | tpo);\n";
-    else
+    if (h.x_mask) {
+      // exported piece s = the output index's top x_j local bits; they may
+      // come from the chunk index, the thread or the register (disjoint bits)
+      o << "    { const u32 sct = (u32)(((cb | tpo) >> " << h.x_shift << ") & " << h.x_mask << "u);\n";
+      for (int r = 0; r < kNReg; r++) {
+        const u64 ro = reg_phys(nlay - 1, r, true);
+        o << "      reinterpret_cast<double2*>(xp.v[sct | " << ((ro >> h.x_shift) & (u64)h.x_mask)
+          << "u])[(cb | tpo) + " << u(ro) << "] = " << A(r) << ";\n";
+      }
+      o << "    }\n";
+    } else {
       o << "    { double2* __restrict__ so = state + (cb | tpo);\n";
-    for (int r = 0; r < kNReg; r++)
-      o << "      so[" << u(reg_phys(nlay - 1, r, true)) << "] = " << A(r) << ";\n";
-    o << "    }\n";
+      for (int r = 0; r < kNReg; r++)
+        o << "      so[" << u(reg_phys(nlay - 1, r, true)) << "] = " << A(r) << ";\n";
+      o << "    }\n";
+    }
     if (use_vtab) o << "    if (tid < " << NV << "u) scnx[tmap[tid]] = nxv;\n    gbar(1u + grp);\n";
     o << "  }\n";
     // peer stores must be performed before the barrier that publishes them

@@ -660,14 +660,11 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
     st.gpos = gpos;
     st.lpos = top;
     // f1: the exchange can ride on the stores of the pass right before it
-    // (no permute or expand in between; a specialised kernel; its output
-    // positions clear of the exported top positions, which then come from
-    // the chunk index and select one destination per chunk)
+    // (no permute or expand in between; a specialised kernel, which picks
+    // each store's destination from the exported top bits of its index)
     if (buf == 0 && !plan.steps.empty() && plan.steps.back().type == Step::PASS) {
       PassPlan& lp = plan.steps.back().pass;
-      bool ok = lp.buf == 0 && lp.kernel != KK_SMALL && lp.nl >= S.cfg->jit_min_qubits;
-      for (int p : lp.opos)
-        if (p >= nl - j) ok = false;
+      const bool ok = lp.buf == 0 && lp.kernel != KK_SMALL && lp.nl >= S.cfg->jit_min_qubits;
       if (ok) {
         lp.x_j = j;
         st.fusable = true;
