@@ -223,6 +223,18 @@ struct Gen {
   std::map<int, int> slot_col;
   bool use_vtab = false;
   size_t sc_cis = 0;  // u64 offset of the cis columns in a shape-sum copy
+  // table rows of <= 32 entries are kept per warp (each warp loads its next
+  // chunk's row, lane t holding entry t, published with __syncwarp): no
+  // CTA-wide barrier per chunk.  ang_col: shape -> its angle column.
+  bool warp_tab = false;
+  std::map<int, int> ang_col;
+  std::string sref(int j) const {
+    if (warp_tab) {
+      auto it = ang_col.find(j);
+      if (it != ang_col.end()) return "wrow[" + std::to_string(it->second) + "]";
+    }
+    return "scoef[" + std::to_string(j) + "]";
+  }
   int nm[kNReg];  // register slot -> variable index (X renames)
   // per-thread factors that multiply every register, not yet applied:
   // folded into the next full-width diagonal's E0, else applied at the store
@@ -267,6 +279,11 @@ struct Gen {
         pool(reinterpret_cast<const double*>(blob + hh.off_pool)) {
     for (int r = 0; r < kNReg; r++) nm[r] = r;
     use_vtab = table_columns(blob, &tc, &slot_col);
+    // (not for diagonal-only passes: there the per-chunk barrier keeps the
+    // CTA's warps on one chunk, which the streaming stores prefer -- A/B:
+    // QFT-30 K2 4.50 -> 3.85 ms, RZZ-30 K3 3.33 -> 3.72 ms with warp rows)
+    warp_tab = use_vtab && tc.width <= 32 && hh.kernel != KK_DIAG && !getenv("QS_JIT_CTATAB");
+    for (int t = 0; t < tc.n_ang; t++) ang_col[tc.ang[t]] = t;
   }
   std::string A(int r) const { return "a" + std::to_string(nm[r]); }
 
@@ -471,10 +488,10 @@ struct Gen {
     std::string s = "0ull";
     for (int j = G.rbeg[R]; j < G.rbeg[R + 1]; j++) {
       const uint32_t tm = shapes[j].tmask;
-      if (tm == 0) s += " + scoef[" + std::to_string(j) + "]";
+      if (tm == 0) s += " + " + sref(j);
       else
-        s += " + (((tid & " + std::to_string(tm) + "u) == " + std::to_string(tm) + "u) ? scoef[" +
-             std::to_string(j) + "] : 0ull)";
+        s += " + (((tid & " + std::to_string(tm) + "u) == " + std::to_string(tm) + "u) ? " + sref(j) +
+             " : 0ull)";
     }
     return s;
   }
@@ -483,10 +500,10 @@ struct Gen {
     std::string s = "0ull";
     for (int j : js) {
       const uint32_t tm = shapes[j].tmask;
-      if (tm == 0) s += " + scoef[" + std::to_string(j) + "]";
+      if (tm == 0) s += " + " + sref(j);
       else
-        s += " + (((tid & " + std::to_string(tm) + "u) == " + std::to_string(tm) + "u) ? scoef[" +
-             std::to_string(j) + "] : 0ull)";
+        s += " + (((tid & " + std::to_string(tm) + "u) == " + std::to_string(tm) + "u) ? " + sref(j) +
+             " : 0ull)";
     }
     return s;
   }
@@ -837,14 +854,17 @@ struct Gen {
     const size_t buf_bytes = (size_t)NB * CH * 16;
     // shape sums; with the per-chunk table, two copies: the chunk's and the
     // group's next chunk's (prefetched during the chunk)
-    const size_t sc_copy = use_vtab ? sc_pad + (2 * tc.n_cis + 2) * 8 : sc_pad;
-    const size_t sc_bytes = use_vtab ? 2 * sc_copy : sc_copy;
+    const size_t sc_copy = (use_vtab && !warp_tab) ? sc_pad + (2 * tc.n_cis + 2) * 8 : sc_pad;
+    const size_t sc_bytes = warp_tab ? sc_pad + (kThreads / 32) * 64 * 8 : use_vtab ? 2 * sc_copy : sc_copy;
     const std::string SCN = std::to_string(sc_copy / 8);
     o << "  const u32 tid = threadIdx.x & 255u;\n";
     o << "  const u32 grp = threadIdx.x >> 8;\n  (void)grp;\n";
     o << "  double2* const bufs = reinterpret_cast<double2*>(smem_raw);\n  (void)bufs;\n";
     o << "  u64* const scbase = reinterpret_cast<u64*>(smem_raw + " << buf_bytes << " + grp * " << sc_bytes << ");\n";
     o << "  u64* scoef = scbase;\n  (void)scoef;\n";
+    if (warp_tab)
+      o << "  u64* const wbase = scbase + " << sc_pad / 8 << " + (tid >> 5) * 64;\n"
+        << "  const u32 lane = tid & 31u;\n";
     const size_t mbar_off = buf_bytes + NG * sc_bytes;
     // issued[b]: loads issued into buffer b so far (two groups: see the wait)
     if (pipe)
@@ -910,7 +930,7 @@ struct Gen {
         o << "        acc += __ldg(trm + 2 * q + 1);\n";
       o << "      }\n"
         << "      for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);\n"
-        << "      if ((tid & 31u) == 0) { scoef[j] = acc;" << (use_vtab && !use_cphys ? " scoef[j + " + SCN + "] = acc;" : "")
+        << "      if ((tid & 31u) == 0) { scoef[j] = acc;" << (use_vtab && !warp_tab && !use_cphys ? " scoef[j + " + SCN + "] = acc;" : "")
         << " }\n    }\n";
     };
     if (!cons.empty()) {
@@ -919,7 +939,10 @@ struct Gen {
       o << "  }\n  __syncthreads();\n";
     }
     const std::string NV = std::to_string(W);
-    if (use_vtab)
+    if (warp_tab)
+      o << "  { const u64 c0 = " << chunk_of("grp") << ";\n    if (lane < " << NV << "u && c0 < " << N
+        << ") wbase[lane] = __ldg(vtab + corder(c0) * " << NV << "ull + lane);\n    __syncwarp(); }\n";
+    else if (use_vtab)
       o << "  { const u64 c0 = " << chunk_of("grp") << ";\n    if (tid < " << NV << "u && c0 < " << N
         << ") scoef[tmap[tid]] = __ldg(vtab + corder(c0) * " << NV << "ull + tid); }\n  __syncthreads();\n";
     o << "  double2 a0, a1, a2, a3, a4, a5, a6, a7, a8, a9, a10, a11, a12, a13, a14, a15;\n";
@@ -942,7 +965,16 @@ struct Gen {
                   count + " }\n";
     o << "    const u64 cb = " << cbexpr << ";\n";
     o << "    const u64 cphys = cb | rank_base;\n    (void)cphys;\n";
-    if (use_vtab) {
+    if (warp_tab) {
+      // per-warp table rows (two copies: this chunk's, the next one's)
+      o << "    const u64* const wrow = wbase + (((k / " << NG << "u) & 1u) ? 32 : 0);\n"
+        << "    u64* const wnx = wbase + (((k / " << NG << "u) & 1u) ? 0 : 32);\n"
+        << "    const double2* const cisv = reinterpret_cast<const double2*>(wrow + " << ((tc.n_ang + 1) & ~1) << ");\n"
+        << "    (void)cisv; (void)wrow;\n"
+        << "    u64 nxv = 0ull;\n"
+        << "    { const u64 nc = " << chunk_of("k + " + std::to_string(NG)) << ";\n"
+        << "      if (lane < " << NV << "u && nc < " << N << ") nxv = __ldg(vtab + corder(nc) * " << NV << "ull + lane); }\n";
+    } else if (use_vtab) {
       // one coalesced table row per chunk instead of the level-1 term loops,
       // loaded one chunk ahead (stored to the other copy at the chunk's end)
       o << "    u64* const scoef = scbase + (((k / " << NG << "u) & 1u) ? " << SCN << " : 0);\n"
@@ -1072,7 +1104,8 @@ struct Gen {
         o << "      so[" << u(reg_phys(nlay - 1, r, true)) << "] = " << A(r) << ";\n";
       o << "    }\n";
     }
-    if (use_vtab) o << "    if (tid < " << NV << "u) scnx[tmap[tid]] = nxv;\n    gbar(1u + grp);\n";
+    if (warp_tab) o << "    if (lane < " << NV << "u) wnx[lane] = nxv;\n    __syncwarp();\n";
+    else if (use_vtab) o << "    if (tid < " << NV << "u) scnx[tmap[tid]] = nxv;\n    gbar(1u + grp);\n";
     o << "  }\n";
     // peer stores must be performed before the barrier that publishes them
     if (h.x_mask) o << "  __threadfence_system();\n";
