@@ -1,7 +1,7 @@
 """bench.py -- driver benchmark of the state-vector hot path on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload qft|rzz|diag|qaoa] [--no-cpu-baseline]
+                    [--workload qft|rzz|diag|qaoa|rand] [--no-cpu-baseline]
 
 One "step" = one pass of the whole hot path over one synthetic input:
 qs_set_basis_state(x) + qs_apply_circuit(circuit) through the C-ABI
@@ -68,6 +68,8 @@ def make_circuit(workload: str, n: int):
         return W.diag_chain(n, 1)
     if workload == "qaoa":
         return W.qaoa_maxcut(n, 4, 1, degree=3 if n % 2 == 0 else 4)
+    if workload == "rand":  # BASELINE configs[4]: supremacy-style, depth 20 (5x7 grid at 35)
+        return W.supremacy(5, 7, 20, 1) if n == 35 else W.supremacy_n(n, 20, 1)
     raise ValueError(workload)
 
 
@@ -190,8 +192,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="qft", choices=["qft", "rzz", "diag", "qaoa"])
-    ap.add_argument("--n", type=int, default=0, help="override qubit count")
+    ap.add_argument("--workload", default="qft", choices=["qft", "rzz", "diag", "qaoa", "rand"])
+    ap.add_argument("--qubits", "--n", dest="n", type=int, default=0,
+                    help="override qubit count (--qubits under torchrun: its parser claims --n)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
