@@ -331,20 +331,32 @@ double2* recv_buffer(qs_ctx* ctx, int d) {
   return ctx->ipc[2 * d + ((ctx->swap_parity & 1) ? 0 : 1)];
 }
 
-// Destination bases of rank r's exported pieces for the swap `st`: piece s
-// of rank r lands in the receive buffer of rank dest(r, s) at piece u(r), so
-// the base is that buffer + (u(r) - s) * 2^(nl-j) amplitudes.
+// Destination bases of rank r's exported pieces for the swap `st`: local
+// index i whose bits at lpos spell s goes to rank dest(r, s), at i with
+// those bits replaced by u(r) -- so the base is that rank's receive buffer
+// + (dep(u(r)) - dep(s)) amplitudes, dep(v) placing bit i of v at lpos[i].
 void fused_targets(qs_ctx* ctx, const Step& st, int r, u64 out[8]) {
   const int j = st.j, nl = ctx->nl;
-  int ur = 0, d0 = r;
+  auto dep = [&](int v) {
+    u64 x = 0;
+    for (int i = 0; i < j; i++) x |= (u64)((v >> i) & 1) << st.lpos[i];
+    return x;
+  };
+  int ur = 0;
   for (int i = 0; i < j; i++) ur |= ((r >> (st.gpos[i] - nl)) & 1) << i;
   for (int s = 0; s < 8; s++) {
     out[s] = 0;
     if (s >= (1 << j)) continue;
-    int d = d0;
+    int d = r;
     for (int i = 0; i < j; i++) d = (d & ~(1 << (st.gpos[i] - nl))) | (((s >> i) & 1) << (st.gpos[i] - nl));
-    out[s] = (u64)recv_buffer(ctx, d) + (((u64)ur << (nl - j)) - ((u64)s << (nl - j))) * sizeof(double2);
+    out[s] = (u64)recv_buffer(ctx, d) + (dep(ur) - dep(s)) * sizeof(double2);
   }
+}
+
+bool top_lpos(const qs_ctx* ctx, const Step& st) {
+  for (int i = 0; i < st.j; i++)
+    if (st.lpos[i] != ctx->nl - st.j + i) return false;
+  return true;
 }
 
 // ----------------------------------------------------------------- swap
@@ -511,9 +523,34 @@ int execute(qs_ctx* ctx, const Plan& plan) {
         }
         for (Shard& sh : ctx->shards) std::swap(sh.state, sh.scratch);
         ctx->n_fused_swaps++;
-      } else {
+      } else if (top_lpos(ctx, st)) {
         rc = exec_swap(ctx, st);
         if (rc) return rc;
+      } else {
+        // a direct swap planned for fusion but run unfused (no peer access):
+        // transpose lpos[i] <-> top[i], swap the top positions, transpose back
+        Step tst = st;
+        std::vector<int> ta, tb;
+        for (int i = 0; i < st.j; i++) {
+          tst.lpos[i] = ctx->nl - st.j + i;
+          if (st.lpos[i] != tst.lpos[i]) ta.push_back(st.lpos[i]), tb.push_back(tst.lpos[i]);
+        }
+        for (int pass = 0; pass < 3; pass++) {
+          if (pass == 1) {
+            rc = exec_swap(ctx, tst);
+            if (rc) return rc;
+            ctx->swap_parity++;
+            continue;
+          }
+          for (Shard& sh : ctx->shards) {
+            CU(cudaSetDevice(sh.device));
+            CU(launch_permute(sh.state, sh.scratch, shard_amps, ta.data(), tb.data(), (int)ta.size(), sh.stream));
+            std::swap(sh.state, sh.scratch);
+            ctx->launches++;
+          }
+          ctx->swap_parity++;
+        }
+        ctx->swap_parity--;  // the step's own increment follows
       }
       ctx->fused_pending = false;
       ctx->swap_parity++;
@@ -645,6 +682,8 @@ int execute(qs_ctx* ctx, const Plan& plan) {
           } else {
             if (!jerr.empty()) ctx->jit_errors++, ctx->jit_last_error = jerr;
             CU(launch_pass(p.kernel, dblob, h, buf, sh.stream));
+            if (fuse && !top_lpos(ctx, plan.steps[k + 1]))
+              return set_err(ctx, QS_EINVAL, "a direct fused swap needs the specialised kernel: " + jerr);
             if (fuse) {
               // interpreter kernels store locally: export the pieces by copies
               const size_t piece = (size_t)1 << h.x_shift;

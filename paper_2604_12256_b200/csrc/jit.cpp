@@ -751,13 +751,31 @@ struct Gen {
     {
       int B = 0;
       while ((1ull << B) < h.n_chunks) B++;
-      int J = 0;
-      while ((1 << J) <= h.x_mask) J++;
-      if (h.x_mask && J <= B)
-        o << "__device__ __forceinline__ u64 corder(u64 c) { return (c >> " << J << ") | ((c & "
-          << h.x_mask << "ull) << " << B - J << "); }\n";
-      else
+      // chunk-id bits that land on exported positions (the non-chunk
+      // positions in ascending order are the chunk id's bits)
+      std::vector<int> nonchunk, dbits;
+      for (int p = 0; p < h.nl; p++) {
+        bool in = false;
+        for (int c = 0; c < kChunkBits; c++)
+          if (h.cpos[c] == p) in = true;
+        if (!in) nonchunk.push_back(p);
+      }
+      for (int i = 0; h.x_mask && (1 << i) <= h.x_mask; i++)
+        for (size_t b = 0; b < nonchunk.size(); b++)
+          if (nonchunk[b] == h.x_pos[i] && (int)b < B) dbits.push_back((int)b);
+      if (dbits.empty()) {
         o << "__device__ __forceinline__ u64 corder(u64 c) { return c; }\n";
+      } else {
+        // loop index bit t < |dbits| -> chunk-id bit dbits[t]; the others in order
+        std::vector<int> src(B, -1);
+        for (size_t t = 0; t < dbits.size(); t++) src[dbits[t]] = (int)t;
+        int next = (int)dbits.size();
+        for (int b = 0; b < B; b++)
+          if (src[b] < 0) src[b] = next++;
+        o << "__device__ __forceinline__ u64 corder(u64 c) { return 0ull";
+        for (int b = 0; b < B; b++) o << " | (((c >> " << src[b] << ") & 1ull) << " << b << ")";
+        o << "; }\n";
+      }
     }
     auto emit_arr = [&](const char* name, const std::vector<int>& v) {
       o << "__device__ const int " << name << "[" << std::max<size_t>(1, v.size()) << "] = {";
@@ -1091,11 +1109,17 @@ struct Gen {
     if (h.x_mask) {
       // exported piece s = the output index's top x_j local bits; they may
       // come from the chunk index, the thread or the register (disjoint bits)
-      o << "    { const u32 sct = (u32)(((cb | tpo) >> " << h.x_shift << ") & " << h.x_mask << "u);\n";
+      int xj = 0;
+      while ((1 << xj) <= h.x_mask) xj++;
+      o << "    { const u64 xi = cb | tpo;\n      const u32 sct = 0u";
+      for (int i = 0; i < xj; i++) o << " | ((u32)((xi >> " << (int)h.x_pos[i] << ") & 1ull) << " << i << ")";
+      o << ";\n";
       for (int r = 0; r < kNReg; r++) {
         const u64 ro = reg_phys(nlay - 1, r, true);
-        o << "      reinterpret_cast<double2*>(xp.v[sct | " << ((ro >> h.x_shift) & (u64)h.x_mask)
-          << "u])[(cb | tpo) + " << u(ro) << "] = " << A(r) << ";\n";
+        u64 sr = 0;
+        for (int i = 0; i < xj; i++) sr |= ((ro >> h.x_pos[i]) & 1ull) << i;
+        o << "      reinterpret_cast<double2*>(xp.v[sct | " << sr << "u])[xi + " << u(ro) << "] = " << A(r)
+          << ";\n";
       }
       o << "    }\n";
     } else {

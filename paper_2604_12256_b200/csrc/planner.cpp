@@ -633,7 +633,28 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
     std::vector<int> victims(cand.begin(), cand.begin() + j);
     std::vector<int> top;
     for (int i = 0; i < j; i++) top.push_back(nl - j + i);
-    {
+    // f1: the exchange can ride on the stores of the pass right before it
+    // (no expand in between; a specialised kernel, which picks each store's
+    // destination from the exported bits of its index).  Then the victims
+    // need not be moved to the top positions first: the swap exchanges the
+    // globals directly with the victims' positions (a victim already on top
+    // pairs with its own top slot, so that the swap equals "permute the
+    // victims to the top, swap, permute back" -- the unfused fallback).
+    PassPlan* fuse_into = nullptr;
+    if (buf == 0 && !plan.steps.empty() && plan.steps.back().type == Step::PASS) {
+      PassPlan& lp = plan.steps.back().pass;
+      if (lp.buf == 0 && lp.kernel != KK_SMALL && lp.nl >= S.cfg->jit_min_qubits) fuse_into = &lp;
+    }
+    static const bool direct_on = !getenv("QS_NO_DIRECT_SWAP");  // A/B knob
+    std::vector<int> lpos = top;
+    if (fuse_into && direct_on) {
+      std::vector<int> rest;
+      for (int v : victims)
+        if (v >= nl - j) lpos[v - (nl - j)] = -1 - v;  // placeholder: fixed below
+        else rest.push_back(v);
+      size_t ri = 0;
+      for (int i = 0; i < j; i++) lpos[i] = (lpos[i] < 0) ? -1 - lpos[i] : rest[ri++];
+    } else {
       // local bit permutation bringing the victims to the top positions
       std::vector<int> tv, vv;  // top non-victims, victims not on top
       for (int t : top)
@@ -652,24 +673,19 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
         plan.steps.push_back(ps);
         plan.stats.n_passes++;
         plan.stats.bytes_hbm += (32ull << nl);
+        fuse_into = nullptr;
       }
     }
     Step st;
     st.type = Step::SWAP;
     st.j = j;
     st.gpos = gpos;
-    st.lpos = top;
-    // f1: the exchange can ride on the stores of the pass right before it
-    // (no permute or expand in between; a specialised kernel, which picks
-    // each store's destination from the exported top bits of its index)
-    if (buf == 0 && !plan.steps.empty() && plan.steps.back().type == Step::PASS) {
-      PassPlan& lp = plan.steps.back().pass;
-      const bool ok = lp.buf == 0 && lp.kernel != KK_SMALL && lp.nl >= S.cfg->jit_min_qubits;
-      if (ok) {
-        lp.x_j = j;
-        st.fusable = true;
-        plan.stats.n_fusable_swaps++;
-      }
+    st.lpos = lpos;
+    if (fuse_into) {
+      fuse_into->x_j = j;
+      fuse_into->x_pos = lpos;
+      st.fusable = true;
+      plan.stats.n_fusable_swaps++;
     }
     // relabel: logical at gpos[i] <-> logical at lpos[i]
     for (int i = 0; i < j; i++) std::swap(map[inv[st.gpos[i]]], map[inv[st.lpos[i]]]);
@@ -867,6 +883,8 @@ int encode_pass(const PassPlan& p, int rank, std::vector<unsigned char>& out, st
   h.scale = 1.0;
   h.x_shift = p.x_j ? p.nl - p.x_j : 0;
   h.x_mask = p.x_j ? (1 << p.x_j) - 1 : 0;
+  memset(h.x_pos, 0, sizeof h.x_pos);
+  for (int i = 0; i < p.x_j; i++) h.x_pos[i] = (int8_t)p.x_pos[i];
   int n_hu = 0;
   std::vector<KOp> kops;
   std::vector<KGroup> kgroups;
@@ -1261,6 +1279,9 @@ std::string plan_to_json(const Plan& plan, bool detail) {
         const PassPlan& p = st.pass;
         o << "\"type\":\"pass\",\"kernel\":\"" << kname(p.kernel) << "\",\"buf\":" << p.buf
           << ",\"nl\":" << p.nl << ",\"src_mode\":" << p.src_mode << ",\"x_j\":" << p.x_j
+          << ",\"x_pos\":[" << (p.x_j > 0 ? std::to_string(p.x_pos[0]) : "")
+          << (p.x_j > 1 ? "," + std::to_string(p.x_pos[1]) : "") << (p.x_j > 2 ? "," + std::to_string(p.x_pos[2]) : "")
+          << "]"
           << ",\"cpos\":[";
         for (size_t k = 0; k < p.cpos.size(); k++) o << (k ? "," : "") << p.cpos[k];
         o << "],\"opos\":[";

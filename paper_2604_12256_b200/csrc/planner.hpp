@@ -60,6 +60,7 @@ struct PassPlan {
   // stores -- output indices whose top x_j local bits are s go straight to the
   // receive buffer of the rank the swap sends piece s to (0: not fused)
   int x_j = 0;
+  std::vector<int> x_pos;     // the swap's local positions (exported bit i)
   // filled by encode_pass
   std::vector<std::vector<int>> phase_regs;  // per phase: chunk bits held in registers
   std::vector<int> op_phase;

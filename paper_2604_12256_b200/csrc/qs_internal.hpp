@@ -120,7 +120,8 @@ struct KPass {
   u64 local_mask;      // (1 << nl) - 1
   u64 basis;           // src_mode 2: physical index of the 1.0 amplitude
   double scale;        // multiplies every amplitude at the store (OP_HU)
-  int32_t x_shift, x_mask;  // fused swap export: dest = (local index >> x_shift) & x_mask
+  int32_t x_shift, x_mask;  // fused swap export: x_mask = 2^j - 1 (0: none)
+  int8_t x_pos[8];          // piece s = sum_i bit x_pos[i] of the local index << i
   int8_t cpos[16];     // physical position of chunk bit c (loads, ops)
   int8_t opos[16];     // physical position of chunk bit c (stores; relabel)
   int8_t run_src[kMaxRuns], run_dst[kMaxRuns], run_len[kMaxRuns];

@@ -142,7 +142,28 @@ def replay_shards(plan: dict, n: int, n_ranks: int, shards=None, subs=None) -> l
         elif ty == "swap":
             j = st["j"]
             bits = [p - nl for p in st["gpos"]]
-            assert st["lpos"] == list(range(nl - j, nl))
+            top = list(range(nl - j, nl))
+            # a swap with non-top local positions (fused swaps, reading r8)
+            # = local transpositions lpos[i] <-> top[i], the top swap, and
+            # the same transpositions again
+            tr = [(a, b) for a, b in zip(st["lpos"], top) if a != b]
+            assert all(a < nl - j for a, _ in tr), "non-top victims pair with free top slots"
+
+            def transpose(shards):
+                if not tr:
+                    return shards
+                idx = np.arange(1 << nl, dtype=np.int64)
+                dst = idx.copy()
+                for a, b in tr:
+                    x = ((idx >> a) ^ (idx >> b)) & 1
+                    dst ^= (x << a) | (x << b)
+                out = []
+                for sh in shards:
+                    o = np.empty_like(sh)
+                    o[dst] = sh
+                    out.append(o)
+                return out
+            shards = transpose(shards)
             piece = 1 << (nl - j)
             new = [np.empty_like(s) for s in shards]
             for r in range(n_ranks):
@@ -152,7 +173,7 @@ def replay_shards(plan: dict, n: int, n_ranks: int, shards=None, subs=None) -> l
                     for i, b in enumerate(bits):
                         d = (d & ~(1 << b)) | (((s >> i) & 1) << b)
                     new[d][ur * piece:(ur + 1) * piece] = shards[r][s * piece:(s + 1) * piece]
-            shards = new
+            shards = transpose(new)
         elif ty == "pass":
             buf = st["buf"]
             ranks = range(n_ranks) if buf == 0 else [0]

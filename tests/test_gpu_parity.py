@@ -210,6 +210,32 @@ def test_loopback_fused_swaps(qs, ranks):
     assert maxdiff(psi2, oracle.apply_circuit(n, W.random_circuit(n, 160, 5 + ranks, diag_bias=0.3), x=3)) < TOL
 
 
+@pytest.mark.parametrize("ranks", [2, 4])
+def test_loopback_direct_swaps_unfused(qs, ranks, monkeypatch):
+    """Swaps planned against the victims' own positions (for fusion) but run
+    without peer stores: transpose, swap the top positions, transpose back."""
+    monkeypatch.setenv("QS_NO_FUSED_SWAP", "1")
+    n = 18
+    gates = W.supremacy_n(n, 8, 3)
+    plan = qs.plan_json(n, gates, n_ranks=ranks, config=qs.make_config(jit_min_qubits=0), detail=True)
+    nl = n - (ranks.bit_length() - 1)
+    assert any(s["type"] == "swap" and s["lpos"] != list(range(nl - s["j"], nl)) for s in plan["steps"])
+    psi, st = sim_run(qs, n, gates, ranks=ranks, jit_min_qubits=0)
+    assert st["n_fused_swaps"] == 0 and st["n_swaps"] >= 1
+    assert maxdiff(psi, oracle.apply_circuit(n, gates)) < TOL
+
+
+@pytest.mark.parametrize("ranks", [2, 4, 8])
+def test_loopback_fused_direct_swaps(qs, ranks):
+    """Supremacy-style circuits: every swap fused, exchanging the globals
+    directly with the victims' positions (no permute passes)."""
+    n = 18
+    gates = W.supremacy_n(n, 10, 5)
+    psi, st = sim_run(qs, n, gates, ranks=ranks, jit_min_qubits=0)
+    assert st["n_swaps"] >= 1 and st["n_fused_swaps"] == st["n_swaps"]
+    assert maxdiff(psi, oracle.apply_circuit(n, gates)) < TOL
+
+
 def test_loopback_qaoa_swaps(qs):
     n = 18
     gates = W.qaoa_maxcut(n, 3, 2)
