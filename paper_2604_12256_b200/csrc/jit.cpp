@@ -146,11 +146,12 @@ namespace {
 bool table_columns(const unsigned char* blob, TabCols* v, std::map<int, int>* slot_col) {
   KPass h;
   memcpy(&h, blob, sizeof h);
+  memset(v, 0, sizeof *v);
+  if (getenv("QS_JIT_NOTAB")) return false;  // tests: force the in-kernel level-1 sums
   const KOp* ops = reinterpret_cast<const KOp*>(blob + h.off_ops);
   const KGroup* groups = reinterpret_cast<const KGroup*>(blob + h.off_groups);
   const KShape* shapes = reinterpret_cast<const KShape*>(blob + h.off_shapes);
   const KTerm* terms = reinterpret_cast<const KTerm*>(blob + h.off_terms);
-  memset(v, 0, sizeof *v);
   auto vary = [&](int j) {
     for (int q = shapes[j].term_begin; q < shapes[j].term_end; q++)
       if (terms[q].ncmask) return true;

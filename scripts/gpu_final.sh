@@ -1,5 +1,9 @@
-# bench (default, with cpu baseline + e2e), launch list, full ncu of the QFT-30 passes
+# parity + smoke + default bench (cpu baseline, e2e) + reference arm + launch list + full ncu of the QFT-30 passes
 cd $GRAFT_REPO_ROOT
+timeout 1500 python -m pytest tests -m gpu -q --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1
 echo "bench rc=$?" >> gpurun_out/bench_default.log
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1

@@ -80,6 +80,18 @@ def test_store_relabel(qs, jit, n):
     assert maxdiff(psi, oracle.apply_circuit(n, gates, x=9)) < TOL
 
 
+@pytest.mark.parametrize("mode", ["QS_JIT_NOTAB", "QS_JIT_CTATAB"])
+def test_specialised_table_modes(qs, mode, monkeypatch):
+    """The specialised kernels' level-1 shape sums: in-kernel (no per-chunk
+    table) and the CTA-wide table row, on chunk/dense/diag passes with
+    chunk-dependent diagonals (the default per-warp rows run everywhere else)."""
+    monkeypatch.setenv(mode, "1")
+    n = 20
+    gates = W.random_circuit(n, 260, 21, diag_bias=0.7, max_generic=3) + W.qft(n)[:60] + W.diag_chain(n, 2, 2)
+    psi, _ = sim_run(qs, n, gates, basis=6, jit_min_qubits=0)
+    assert maxdiff(psi, oracle.apply_circuit(n, gates, x=6)) < TOL
+
+
 @pytest.mark.parametrize("jit", [0, 99])
 @pytest.mark.parametrize("n,seed", [(13, 10), (15, 11), (17, 12)])
 def test_specialised_vs_interpreter_kernels(qs, jit, n, seed):
