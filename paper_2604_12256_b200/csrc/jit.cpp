@@ -116,6 +116,10 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(sa(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_group0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(sa(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 // the mbarrier sees one arrival once all of this thread's prior cp.async land
 __device__ __forceinline__ void cp_async_mbar_arrive(u64* b) {
@@ -984,15 +988,27 @@ struct Gen {
                   count + " }\n";
     o << "    const u64 cb = " << cbexpr << ";\n";
     o << "    const u64 cphys = cb | rank_base;\n    (void)cphys;\n";
+    // (cp.async row prefetch unless the pass's own chunk refill uses
+    // per-thread cp.async, whose uncommitted copies a row group would absorb;
+    // A/B on one box: diag-chain-30 K2 6.26 -> 5.09 ms, QFT-30 K2 3.84 ->
+    // 3.91 ms.  Tried for the CTA-wide rows too: RZZ-30 K3 3.33 -> 3.36 ms)
+    const bool row_async = warp_tab && (!pipe || use_tma) && !getenv("QS_JIT_ROWREG");  // env: A/B knob
     if (warp_tab) {
       // per-warp table rows (two copies: this chunk's, the next one's)
+      o << "    u64 nxrow = 0ull;\n    (void)nxrow;\n";
       o << "    const u64* const wrow = wbase + (((k / " << NG << "u) & 1u) ? 32 : 0);\n"
         << "    u64* const wnx = wbase + (((k / " << NG << "u) & 1u) ? 0 : 32);\n"
         << "    const double2* const cisv = reinterpret_cast<const double2*>(wrow + " << ((tc.n_ang + 1) & ~1) << ");\n"
         << "    (void)cisv; (void)wrow;\n"
-        << "    u64 nxv = 0ull;\n"
-        << "    { const u64 nc = " << chunk_of("k + " + std::to_string(NG)) << ";\n"
-        << "      if (lane < " << NV << "u && nc < " << N << ") nxv = __ldg(vtab + corder(nc) * " << NV << "ull + lane); }\n";
+        << "    { const u64 nc = " << chunk_of("k + " + std::to_string(NG)) << ";\n";
+      if (row_async)
+        // the next row goes straight into the other copy with cp.async (a
+        // register load gets sunk by the compiler next to its use)
+        o << "      if (lane < " << NV << "u && nc < " << N << ") cp_async8(wnx + lane, vtab + corder(nc) * " << NV
+          << "ull + lane);\n      cp_async_commit(); }\n";
+      else
+        o << "      u64 nxv = 0ull;\n      if (lane < " << NV << "u && nc < " << N << ") nxv = __ldg(vtab + corder(nc) * "
+          << NV << "ull + lane);\n      nxrow = nxv; }\n";
     } else if (use_vtab) {
       // one coalesced table row per chunk instead of the level-1 term loops,
       // loaded one chunk ahead (stored to the other copy at the chunk's end)
@@ -1129,7 +1145,8 @@ struct Gen {
         o << "      so[" << u(reg_phys(nlay - 1, r, true)) << "] = " << A(r) << ";\n";
       o << "    }\n";
     }
-    if (warp_tab) o << "    if (lane < " << NV << "u) wnx[lane] = nxv;\n    __syncwarp();\n";
+    if (warp_tab && row_async) o << "    cp_async_wait_group0();\n    __syncwarp();\n";
+    else if (warp_tab) o << "    if (lane < " << NV << "u) wnx[lane] = nxrow;\n    __syncwarp();\n";
     else if (use_vtab) o << "    if (tid < " << NV << "u) scnx[tmap[tid]] = nxv;\n    gbar(1u + grp);\n";
     o << "  }\n";
     // peer stores must be performed before the barrier that publishes them

@@ -1,9 +1,9 @@
 cd $GRAFT_REPO_ROOT
-timeout 1200 python -m pytest tests -m gpu -q -x --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -x --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 for i in 1 2; do
-for V in "QS_JIT_CTATAB=1" "QS_WARPTAB=1"; do
-  for w in qft diag rzz qaoa; do
+for V in "QS_JIT_ROWREG=1" "QS_ROWASYNC=1"; do
+  for w in rzz qft; do
   env $V timeout 300 python bench.py --workload $w --steps 3 --warmup 2 --no-cpu-baseline --e2e-steps 0 > "gpurun_out/ab_${V}_${w}_$i.log" 2>&1
   done
 done; done
