@@ -279,6 +279,21 @@ def main():
     bytes_per_step = st["bytes_hbm"] * world
     value = bytes_per_step / (ms * 1e-3) / 1e9
 
+    # global<->local exchanges (K4): NVLink bytes each GPU sends per step;
+    # fused swaps ride on the preceding pass's stores (their time is inside
+    # that pass), so only unfused swaps have an exchange time of their own
+    nvl = None
+    if world > 1 and st["n_swaps"]:
+        sw = kt.get("K4_swap", {"ms": 0.0})
+        unf = st["n_swaps"] - st["n_fused_swaps"]
+        nvl = {"bytes_per_gpu_per_step": st["bytes_nvlink"], "swaps": st["n_swaps"],
+               "fused_swaps": st["n_fused_swaps"], "swap_step_ms": sw["ms"] / args.steps,
+               "peak_gbs_per_direction": 900.0,
+               "note": "fused swaps: exchange overlapped with the pass (peer stores); swap_step_ms is "
+                       "then only the barrier" if unf == 0 else "NCCL grouped send/recv"}
+        if unf == st["n_swaps"] and sw["ms"] > 0:
+            nvl["achieved_gbs"] = st["bytes_nvlink"] / (sw["ms"] / args.steps * 1e-3) / 1e9
+
     # dominant kernel (largest device time) -> roofline
     dom = max(kt.items(), key=lambda kv: kv[1]["ms"])
     peak, peak_src = measured_peaks()
@@ -351,7 +366,7 @@ def main():
                                         "n_diag_passes", "n_swaps", "n_expand",
                                         "n_substate_gates", "n_fused_diag", "bytes_hbm")},
             "kernels": {k: v for k, v in kt.items() if v["launches"]},
-            "roofline": roof, "cpu_baseline": base, "e2e": e2e,
+            "roofline": roof, "cpu_baseline": base, "e2e": e2e, "nvlink": nvl,
             "gpu_launches": launches, "clocks": clk,
         }
         print(json.dumps(line), flush=True)
