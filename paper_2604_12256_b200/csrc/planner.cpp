@@ -360,7 +360,7 @@ static void assign_phases(PassPlan& p) {
 }
 
 static void finalize_chunk_pass(Sched& S, PassPlan& p, u64 need_pos, int nl,
-                                std::vector<int>* map) {
+                                std::vector<int>* map, const std::vector<IrGate>* upcoming) {
   const int m = kChunkBits;
   // chunk positions: the needed ones, filled with the lowest free positions
   u64 c = need_pos;
@@ -424,6 +424,54 @@ static void finalize_chunk_pass(Sched& S, PassPlan& p, u64 need_pos, int nl,
       }
       mp.swap(moved);
       p.opos = opos;
+    }
+  }
+  // Low-slot steering (reading r7): the 3 lowest positions are in every
+  // chunk, so every pass can act on the qubits that sit there.  The store
+  // puts there, among the qubits the last layout keeps on lane bits (so the
+  // 128 B store runs stay coalesced), those whose next dense gate comes
+  // soonest; the map records the relabel.
+  static const bool steer_on = !getenv("QS_NO_LOW_STEER");  // A/B knob
+  if (map && upcoming && steer_on && p.cpos.size() >= 3 && p.cpos[0] == 0 && p.cpos[1] == 1 &&
+      p.cpos[2] == 2) {
+    std::vector<int>& mp = *map;  // logical -> physical, already after the store relabel
+    const std::vector<int> order = phase_thread_order(p.phase_regs.back(), (int)p.cpos.size());
+    const int nlane = std::min<int>(5, (int)order.size());
+    // output position -> logical qubit (for this chunk's qubits)
+    auto qubit_at = [&](int pos) {
+      for (size_t q = 0; q < mp.size(); q++)
+        if (mp[q] == pos) return (int)q;
+      return -1;
+    };
+    auto next_use = [&](int q) {
+      for (size_t i = 0; i < upcoming->size(); i++) {
+        const IrGate& g = (*upcoming)[i];
+        if (g.type != IrGate::DENSE) continue;
+        for (int t : g.targets)
+          if (t == q) return (long)i;
+      }
+      return (long)1 << 40;
+    };
+    struct Cand { int c; long use; };
+    std::vector<Cand> cand;
+    for (int t = 0; t < nlane; t++) {
+      const int c = order[t];
+      const int q = qubit_at(p.opos[c]);
+      cand.push_back({c, q >= 0 ? next_use(q) : ((long)1 << 41)});
+    }
+    std::stable_sort(cand.begin(), cand.end(), [](const Cand& a, const Cand& b) { return a.use < b.use; });
+    // give output positions 0,1,2 to the 3 best lane-bit chunk bits; the
+    // chunk bits that fed them take the vacated positions
+    for (int slot = 0; slot < 3; slot++) {
+      const int c = cand[slot].c;
+      if (p.opos[c] == slot) continue;
+      int holder = -1;
+      for (size_t k = 0; k < p.opos.size(); k++)
+        if (p.opos[k] == slot) holder = (int)k;
+      const int qa = qubit_at(p.opos[c]), qb = qubit_at(slot);
+      std::swap(p.opos[c], p.opos[holder]);
+      if (qa >= 0) mp[qa] = slot;
+      if (qb >= 0) mp[qb] = p.opos[holder];
     }
   }
   if (S.src_mode && p.buf == 0) {
@@ -566,7 +614,7 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
         p.kernel = KK_SMALL;
         p.cpos.clear();
       } else {
-        finalize_chunk_pass(S, p, need, nl, buf == 0 ? &map : nullptr);
+        finalize_chunk_pass(S, p, need, nl, buf == 0 ? &map : nullptr, &deferred);
       }
       plan.steps.push_back(Step{Step::PASS, p});
       if (buf == 0) {  // statistics count full-state passes only
