@@ -303,8 +303,9 @@ def main():
         per_launch = dom[1]["bytes"] / dom[1]["launches"]
         ach = per_launch / (avg_ms * 1e-3) / 1e9
         if dom[0] == "K4_swap":
-            roof = {"kernel": dom[0], "bound": "nvlink", "achieved": ach, "peak": 770.0,
-                    "unit": "GB/s", "frac": ach / 770.0, "traffic": None}
+            roof = {"kernel": dom[0], "bound": "nvlink", "achieved": ach, "peak": 900.0,
+                    "peak_source": "NVLink 5 spec, per direction per GPU (no measured NVLink peak on file)",
+                    "unit": "GB/s", "frac": ach / 900.0, "traffic": None}
         else:
             roof = {"kernel": dom[0], "bound": "hbm", "achieved": ach, "peak": peak,
                     "peak_source": peak_src + " (MEASURED_PEAKS.json hbm_gbs, burst copy)",
