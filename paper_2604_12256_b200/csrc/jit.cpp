@@ -826,7 +826,10 @@ struct Gen {
     // conflict; for run >= 2 the chunk is instead copied with coalesced
     // per-thread cp.async in linear order into XOR-swizzled slots (the
     // exchange layout), conflict-free on both sides.
-    const bool use_tma = pipe && l >= 5 && low_run(L[0]) <= 1 && !getenv("QS_JIT_NOTMA");
+    // (bulk copies of 128 B runs are far slower than per-thread cp.async:
+    // A/B with QS_JIT_TMA_L=3, QAOA-30 155 ms vs 90 ms, rand30 587 vs 333 ms)
+    static const int tma_min_l = getenv("QS_JIT_TMA_L") ? atoi(getenv("QS_JIT_TMA_L")) : 5;  // A/B knob
+    const bool use_tma = pipe && l >= tma_min_l && low_run(L[0]) <= 1 && !getenv("QS_JIT_NOTMA");
     if (use_tma) {
       o << "__device__ __forceinline__ void issue(const double2* __restrict__ state, u64 chunk, double2* dst, u64* bar, u32 lane) {\n"
         << "  const u64 cb = " << cbexpr << ";\n"
