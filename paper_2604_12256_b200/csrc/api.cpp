@@ -415,6 +415,8 @@ int exec_swap(qs_ctx* ctx, const Step& st) {
 
 // -------------------------------------------------------------- execute
 int execute(qs_ctx* ctx, const Plan& plan) {
+  ctx->n_fused_swaps = 0;  // per call (qs_stats_t reports the last call)
+  ctx->fused_pending = false;
   // sub-state pool
   std::vector<size_t> sub_off(plan.subs.size() + 1, 0);
   size_t sub_total = 0;

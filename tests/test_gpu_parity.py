@@ -246,6 +246,15 @@ def test_loopback_fused_direct_swaps(qs, ranks):
     psi, st = sim_run(qs, n, gates, ranks=ranks, jit_min_qubits=0)
     assert st["n_swaps"] >= 1 and st["n_fused_swaps"] == st["n_swaps"]
     assert maxdiff(psi, oracle.apply_circuit(n, gates)) < TOL
+    # the counters are per call
+    s = qs.Simulator(n, loopback_ranks=ranks)
+    s.set_config(qs.make_config(jit_min_qubits=0))
+    for _ in range(2):
+        s.set_basis_state(0)
+        s.apply(gates)
+        st2 = s.stats()
+        assert st2["n_fused_swaps"] == st2["n_swaps"] == st["n_swaps"]
+    s.close()
 
 
 def test_loopback_qaoa_swaps(qs):
