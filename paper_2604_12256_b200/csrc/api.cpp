@@ -353,6 +353,31 @@ void fused_targets(qs_ctx* ctx, const Step& st, int r, u64 out[8]) {
   }
 }
 
+// Device-side barrier over every shard's stream (rank mode: a 1-element
+// NCCL all-reduce; in-process: each stream waits for the others' events).
+int shard_barrier(qs_ctx* ctx) {
+  if (ctx->mode == M_RANK) {
+    for (Shard& sh : ctx->shards) {
+      CU(cudaSetDevice(sh.device));
+      NC(ncclAllReduce(sh.bar, sh.bar, 1, ncclDouble, ncclSum, sh.comm, sh.stream));
+    }
+    return QS_OK;
+  }
+  if (ctx->shards.size() < 2) return QS_OK;
+  std::vector<cudaEvent_t> done;
+  for (Shard& sh : ctx->shards) {
+    CU(cudaSetDevice(sh.device));
+    done.push_back(get_event(sh));
+    CU(cudaEventRecord(done.back(), sh.stream));
+  }
+  for (size_t t = 0; t < ctx->shards.size(); t++) {
+    CU(cudaSetDevice(ctx->shards[t].device));
+    for (size_t u = 0; u < done.size(); u++)
+      if (u != t) CU(cudaStreamWaitEvent(ctx->shards[t].stream, done[u], 0));
+  }
+  return QS_OK;
+}
+
 bool top_lpos(const qs_ctx* ctx, const Step& st) {
   for (int i = 0; i < st.j; i++)
     if (st.lpos[i] != ctx->nl - st.j + i) return false;
@@ -505,24 +530,8 @@ int execute(qs_ctx* ctx, const Plan& plan) {
       if (st.fusable && ctx->fused_pending) {
         // the preceding pass already stored every piece in its destination's
         // receive buffer: wait for all of them, then the buffers trade roles
-        if (ctx->mode == M_RANK) {
-          for (Shard& sh : ctx->shards) {
-            CU(cudaSetDevice(sh.device));
-            NC(ncclAllReduce(sh.bar, sh.bar, 1, ncclDouble, ncclSum, sh.comm, sh.stream));
-          }
-        } else {
-          std::vector<cudaEvent_t> done;
-          for (Shard& sh : ctx->shards) {
-            CU(cudaSetDevice(sh.device));
-            done.push_back(get_event(sh));
-            CU(cudaEventRecord(done.back(), sh.stream));
-          }
-          for (size_t t = 0; t < ctx->shards.size(); t++) {
-            CU(cudaSetDevice(ctx->shards[t].device));
-            for (size_t u = 0; u < done.size(); u++)
-              if (u != t) CU(cudaStreamWaitEvent(ctx->shards[t].stream, done[u], 0));
-          }
-        }
+        rc = shard_barrier(ctx);
+        if (rc) return rc;
         for (Shard& sh : ctx->shards) std::swap(sh.state, sh.scratch);
         ctx->n_fused_swaps++;
       } else if (top_lpos(ctx, st)) {
@@ -562,6 +571,15 @@ int execute(qs_ctx* ctx, const Plan& plan) {
         s0.timed.push_back({KK_SWAP, a, b, (uint64_t)((16ull << ctx->nl) - (16ull << (ctx->nl - st.j)))});
       }
       continue;
+    }
+    // A pass that stores into its peers' receive buffers may only start
+    // once every peer is done with all earlier steps (an unfused swap's
+    // local copy or a permute may still read the buffer that is now the
+    // peer's receive buffer).
+    if (st.type == Step::PASS && st.pass.x_j && k + 1 < plan.steps.size() &&
+        plan.steps[k + 1].type == Step::SWAP && plan.steps[k + 1].fusable && ensure_peers(ctx) == 1) {
+      rc = shard_barrier(ctx);
+      if (rc) return rc;
     }
     for (size_t si = 0; si < ctx->shards.size(); si++) {
       Shard& sh = ctx->shards[si];
