@@ -379,3 +379,39 @@ def test_qft30_sampled_closed_form(qs):
         want = np.exp(2j * math.pi * ((x * k) % (1 << n)) / (1 << n)) / math.sqrt(1 << n)
         assert maxdiff(got, want) < 1e-12
     s.close()
+
+
+def _norm(sim, n, slab=1 << 24):
+    buf = np.empty(slab, dtype=np.float64)
+    tot = 0.0
+    for off in range(0, 1 << n, slab):
+        tot += float(sim.probabilities(off, slab, out=buf).sum())
+    return tot
+
+
+@pytest.mark.parametrize("workload", ["rzz", "diag", "qaoa", "rand"])
+def test_bench_workloads_30_properties(qs, workload):
+    """The other bench workloads at their full size (30 qubits, the launch
+    configuration bench.py times), checked through properties that hold at
+    any size: norm 1 (all 2^30 probabilities summed); RZZ after H^n is a pure
+    phase pattern, |a| = 2^-15 everywhere sampled; MaxCut QAOA is symmetric
+    under flipping every qubit, a(x) = a(~x)."""
+    import bench
+    n = 30
+    gates = bench.make_circuit(workload, n)
+    s = qs.Simulator(n)
+    s.apply(gates)
+    assert abs(_norm(s, n) - 1.0) < 1e-10
+    rng = np.random.default_rng(3)
+    offs = [int(o) for o in rng.integers(0, (1 << n) - 4096, size=6)]
+    if workload == "rzz":
+        for off in offs:
+            got = s.state(off, 4096)
+            assert np.max(np.abs(np.abs(got) - 2.0 ** (-n / 2))) < 1e-12
+    if workload == "qaoa":
+        full = (1 << n) - 1
+        for off in offs:
+            a = s.state(off, 4096)
+            b = s.state(full - off - 4095, 4096)[::-1]   # indices full - x
+            assert maxdiff(a, b) < 1e-12
+    s.close()
