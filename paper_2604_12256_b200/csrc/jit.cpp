@@ -810,6 +810,29 @@ struct Gen {
     // Load passes stream their chunks through two shared-memory stages filled
     // by cp.async.bulk (the TMA bulk-copy engine) one chunk ahead.
     const bool pipe = (h.src_mode == 0);
+    // Loop-invariant expand factors.  A CTA's chunks are blockIdx.x + k *
+    // gridDim.x: when gridDim.x is a multiple of 2^b, chunk-id bits below b
+    // are the same for all of them.  If the positions a register-dependent
+    // booster sub-state reads come only from the chunk bits, those chunk-id
+    // bits and the rank, every thread gathers the same 16 values for every
+    // chunk: they are loaded once into the thread's shared-memory slots (a
+    // runtime check of gridDim.x keeps the per-chunk gather as fallback).
+    int xh_g = -1, xh_b = 0;
+    if (h.src_mode == 1 && nlay == 1 && h.x_mask == 0 && !getenv("QS_JIT_NOXH")) {  // env: A/B knob
+      u64 regpos = 0;
+      for (int r = 0; r < kNReg; r++) regpos |= reg_phys(0, r, false);
+      for (int g = 0; g < h.expand.n && xh_g < 0; g++) {
+        const int glo = h.expand.lo[g], ghi = h.expand.lo[g] + h.expand.len[g];
+        if (!(regpos & (((1ull << h.expand.len[g]) - 1) << glo))) continue;
+        int b = 0;
+        for (int i = 0; i < h.n_runs; i++)
+          for (int t = 0; t < h.run_len[i]; t++) {
+            const int pos = h.run_dst[i] + t;
+            if (pos >= glo && pos < ghi) b = std::max(b, h.run_src[i] + t + 1);
+          }
+        if (b <= 3) xh_g = g, xh_b = b;  // grids are 2 x 148 CTAs = 8 x 37
+      }
+    }
     const int CH = 1 << kChunkBits;
     int l = 0;
     while (l < kChunkBits && h.cpos[l] == l) l++;
@@ -898,6 +921,8 @@ struct Gen {
         << "  volatile u32* issued = reinterpret_cast<volatile u32*>(smem_raw + " << mbar_off + NB * 8
         << ");\n  (void)issued;\n";
     hz_off = mbar_off + (pipe ? ((NB * 12 + 15) / 16) * 16 : 0);
+    const size_t xh_off = hz_off;
+    if (xh_g >= 0) hz_off += (size_t)kNReg * kThreads * 16;
     // hoisted per-thread values (shared by the groups: they depend on tid only)
     // fill what shared memory is left: 227 KB per CTA (two CTAs per SM: half
     // of 228 KB, less the per-CTA reservation), minus the 4 KB sincos table
@@ -971,6 +996,20 @@ struct Gen {
     else if (use_vtab)
       o << "  { const u64 c0 = " << chunk_of("grp") << ";\n    if (tid < " << NV << "u && c0 < " << N
         << ") scoef[tmap[tid]] = __ldg(vtab + corder(c0) * " << NV << "ull + tid); }\n  __syncthreads();\n";
+    if (xh_g >= 0) {
+      const int g = xh_g;
+      o << "  double2* const xh = reinterpret_cast<double2*>(smem_raw + " << xh_off << ");\n"
+        << "  const bool xinv = (gridDim.x & " << ((1u << xh_b) - 1) << "u) == 0u;\n"
+        << "  if (xinv) {\n"
+        << "    const double2* __restrict__ xsv = reinterpret_cast<const double2*>(*reinterpret_cast<const u64*>(blob + "
+        << (size_t)((const unsigned char*)&h.expand.ptr[g] - (const unsigned char*)&h) << "));\n"
+        << "    const u64 chunk = corder(" << chunk_of("grp") << ");\n"
+        << "    const u64 xph = (" << cbexpr << ") | rank_base | tp0;\n";
+      for (int r = 0; r < kNReg; r++)
+        o << "    xh[" << r * kThreads << " + tid] = __ldg(xsv + (((xph | " << u(reg_phys(0, r, false)) << ") >> "
+          << h.expand.lo[g] << ") & " << u((1ull << h.expand.len[g]) - 1) << "));\n";
+      o << "  }\n";
+    }
     o << "  double2 a0, a1, a2, a3, a4, a5, a6, a7, a8, a9, a10, a11, a12, a13, a14, a15;\n";
     const size_t loop_pos = o.str().size();  // hoisted code goes here
     o << "  for (u32 k = grp;; k += " << NG << "u) {\n"
@@ -1069,6 +1108,7 @@ struct Gen {
           const int g = varying[i];
           std::string ld = "__ldg(sv" + std::to_string(g) + " + ((ph >> " + std::to_string(h.expand.lo[g]) +
                            ") & " + u((1ull << h.expand.len[g]) - 1) + "))";
+          if (g == xh_g) ld = "(xinv ? xh[" + std::to_string(r * kThreads) + " + tid] : " + ld + ")";
           if (i == 0) o << ld;
           else o << "; v = cmul(v, " << ld << ")";
         }
