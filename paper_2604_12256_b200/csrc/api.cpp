@@ -40,8 +40,8 @@ cudaError_t launch_gather(const double2* state, double2* out, u64 off, u64 count
 bool jit_prepare(const unsigned char* blob, int device, void** fn_out, int* grid_per_sm,
                  size_t* smem_out, std::string& err, bool compile_only);
 cudaError_t jit_launch(void* fn, int grid, size_t smem, const unsigned char* dblob,
-                       double2* state, u64 rank_base, const u64* vtab, const u64* xpeer8,
-                       const void* pool_host, size_t pool_bytes, cudaStream_t st);
+                       const unsigned char* hblob, double2* state, u64 rank_base, const u64* vtab,
+                       const u64* xpeer8, const void* pool_host, size_t pool_bytes, cudaStream_t st);
 int jit_table_cols(const unsigned char* blob, TabCols* v);
 cudaError_t launch_shape_table(const unsigned char* dblob, u64* tab, u64 rank_base, u64 n_chunks,
                                const TabCols& v, cudaStream_t st);
@@ -696,7 +696,7 @@ int execute(qs_ctx* ctx, const Plan& plan) {
               CU(launch_shape_table(dblob, sh.vtab, h.rank_base, h.n_chunks, vl, sh.stream));
               ctx->launches++;
             }
-            CU(jit_launch(fn, (int)grid, smem, dblob, buf, h.rank_base, sh.vtab, xp, hb + h.off_pool,
+            CU(jit_launch(fn, (int)grid, smem, dblob, hb, buf, h.rank_base, sh.vtab, xp, hb + h.off_pool,
                           pb, sh.stream));
             ctx->jit_launches++;
           } else {

@@ -215,6 +215,41 @@ bool table_columns(const unsigned char* blob, TabCols* v, std::map<int, int>* sl
   return true;
 }
 
+// TMA tensor view of a load pass whose chunk has short contiguous runs
+// (l < 5, where per-run bulk copies lose): the shard as a <= 5-d float64
+// tensor whose dims are the runs of consecutive positions (chunk and
+// non-chunk runs alternate; runs longer than 8 bits split), dim 0 being the
+// low chunk run in doubles.  One cp.async.bulk.tensor per chunk, box = the
+// chunk dims in full and 1 along the others; the smem image is the linear
+// chunk-index layout, like the bulk stage.
+struct TPlan {
+  int rank = 0;
+  int pos[5], len[5];
+  bool chunk[5];
+};
+bool tensor_plan(const KPass& h, TPlan* t) {
+  if (getenv("QS_JIT_NOTENSOR")) return false;  // A/B knob
+  u64 cm = 0;
+  for (int c = 0; c < kChunkBits; c++) cm |= 1ull << h.cpos[c];
+  int l = 0;
+  while (l < kChunkBits && h.cpos[l] == l) l++;
+  if (l < 3 || l >= 5) return false;
+  t->rank = 0;
+  int p = 0;
+  while (p < h.nl) {
+    const bool in = (cm >> p) & 1;
+    int q = p;
+    while (q < h.nl && (((cm >> q) & 1) != 0) == in && (!in || q - p < 8)) q++;
+    if (t->rank == 5) return false;
+    t->pos[t->rank] = p;
+    t->len[t->rank] = q - p;
+    t->chunk[t->rank] = in;
+    t->rank++;
+    p = q;
+  }
+  return t->chunk[0] && t->pos[0] == 0 && t->len[0] == l;
+}
+
 struct Gen {
   std::ostringstream o;
   const KPass& h;
@@ -852,9 +887,28 @@ struct Gen {
     // (bulk copies of 128 B runs are far slower than per-thread cp.async:
     // A/B with QS_JIT_TMA_L=3, QAOA-30 155 ms vs 90 ms, rand30 587 vs 333 ms)
     static const int tma_min_l = getenv("QS_JIT_TMA_L") ? atoi(getenv("QS_JIT_TMA_L")) : 5;  // A/B knob
-    const bool use_tma = pipe && l >= tma_min_l && low_run(L[0]) <= 1 && !getenv("QS_JIT_NOTMA");
-    if (use_tma) {
-      o << "__device__ __forceinline__ void issue(const double2* __restrict__ state, u64 chunk, double2* dst, u64* bar, u32 lane) {\n"
+    TPlan tp;
+    const bool use_tensor = pipe && l < tma_min_l && low_run(L[0]) <= 1 && tensor_plan(h, &tp);
+    const bool use_tma = (pipe && l >= tma_min_l && low_run(L[0]) <= 1 && !getenv("QS_JIT_NOTMA")) || use_tensor;
+    o << "struct __align__(64) QsTmap { u64 v[16]; };\n";
+    if (use_tensor) {
+      // one tensor copy per chunk (coordinates: the non-chunk runs' index bits)
+      o << "__device__ __forceinline__ void issue(const double2* __restrict__ state, u64 chunk, double2* dst, u64* bar, u32 lane, const QsTmap* tm) {\n"
+        << "  (void)state;\n"
+        << "  if (lane == 0) {\n"
+        << "    const u64 cb = " << cbexpr << ";\n"
+        << "    mbar_expect(bar, " << CH * 16 << "u);\n"
+        << "    asm volatile(\"cp.async.bulk.tensor." << tp.rank << "d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {";
+      for (int d = 0; d < tp.rank; d++) o << (d ? ", " : "") << "%" << d + 2;
+      o << "}], [" << "%" << tp.rank + 2 << "];\"\n      :: \"r\"(sa(dst)), \"l\"(tm)";
+      for (int d = 0; d < tp.rank; d++) {
+        if (tp.chunk[d]) o << ", \"r\"(0)";
+        else o << ", \"r\"((u32)((cb >> " << tp.pos[d] << ") & " << ((1ull << tp.len[d]) - 1) << "ull))";
+      }
+      o << ", \"r\"(sa(bar)) : \"memory\");\n  }\n  __syncwarp();\n}\n";
+    } else if (use_tma) {
+      o << "__device__ __forceinline__ void issue(const double2* __restrict__ state, u64 chunk, double2* dst, u64* bar, u32 lane, const QsTmap* tm) {\n"
+        << "  (void)tm;\n"
         << "  const u64 cb = " << cbexpr << ";\n"
         << "  if (lane == 0) mbar_expect(bar, " << CH * 16 << "u);\n"
         << "  __syncwarp();\n"
@@ -897,7 +951,7 @@ struct Gen {
     o << "extern \"C\" __global__ void __launch_bounds__(" << nthreads << ", " << (NG == 1 && NB <= 1 ? 2 : 1)
       << ")\n" << kname
       << "(const unsigned char* __restrict__ blob, double2* __restrict__ state, u64 rank_base, "
-         "const u64* __restrict__ vtab, const QsXPeer xp"
+         "const u64* __restrict__ vtab, const QsXPeer xp, const __grid_constant__ QsTmap tmap"
       << (param_pool ? ", const QsPool P" : "") << ") {\n";
     o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n";
     const size_t buf_bytes = (size_t)NB * CH * 16;
@@ -956,7 +1010,7 @@ struct Gen {
       o << "  const int tcl0 = " << tc_expr(0) << ";\n";
       o << "  for (u32 k = grp; k < " << NB << "u; k += " << NG << "u)\n"
         << "    if (tid < 32 && " << chunk_of("k") << " < " << N << ") { issue(state, corder(" << chunk_of("k") << ")"
-        << ", bufs + k * " << CH << ", mbar + k, tid); if (tid == 0) issued[k] = 1u; }\n";
+        << ", bufs + k * " << CH << ", mbar + k, tid, &tmap); if (tid == 0) issued[k] = 1u; }\n";
     } else if (pipe) {
       std::string tpd = "(0ull";
       for (int i = 0; i < kLogT; i++)
@@ -1024,7 +1078,7 @@ struct Gen {
     const std::string refill =
         use_tma ? "    gbar(1u + grp);  // every thread is done reading the buffer\n"
                   "    if (tid < 32 && " + nxt + " < " + N +
-                  ") { fence_proxy_async(); issue(state, corder(" + nxt + "), sch, mbar + kb, tid); " + count + " }\n"
+                  ") { fence_proxy_async(); issue(state, corder(" + nxt + "), sch, mbar + kb, tid, &tmap); " + count + " }\n"
                 : "    gbar(1u + grp);  // every thread is done reading the buffer\n"
                   "    if (" + nxt + " < " + N + ") { issue_async(state, corder(" + nxt + "), sch, mbar + kb, tpd, sd); " +
                   count + " }\n";
@@ -1220,6 +1274,10 @@ typedef CUresult (*PFN_LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, u
                                      unsigned, unsigned, CUstream, void**, void**);
 typedef CUresult (*PFN_FuncSetAttribute)(CUfunction, CUfunction_attribute, int);
 typedef CUresult (*PFN_OccupancyMax)(int*, CUfunction, int, size_t);
+typedef CUresult (*PFN_TensorMapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                             const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                             const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 struct Driver {
   bool ok = false;
@@ -1228,6 +1286,7 @@ struct Driver {
   PFN_LaunchKernel launch = nullptr;
   PFN_FuncSetAttribute setattr = nullptr;
   PFN_OccupancyMax occ = nullptr;
+  PFN_TensorMapEncodeTiled tmap = nullptr;
 };
 
 Driver& driver() {
@@ -1243,6 +1302,7 @@ Driver& driver() {
            get("cuLaunchKernel", (void**)&d.launch) &&
            get("cuFuncSetAttribute", (void**)&d.setattr) &&
            get("cuOccupancyMaxActiveBlocksPerMultiprocessor", (void**)&d.occ);
+    if (d.ok && !get("cuTensorMapEncodeTiled", (void**)&d.tmap)) d.tmap = nullptr;
   });
   return d;
 }
@@ -1435,9 +1495,41 @@ int jit_table_cols(const unsigned char* blob, TabCols* v) {
   return table_columns(blob, v, nullptr) ? v->width : 0;
 }
 
+// The tensor map of a pass that loads through cp.async.bulk.tensor (see
+// tensor_plan; the same conditions as the generator).  false: not such a
+// pass (out is zeroed).
+bool jit_tensor_map(const unsigned char* blob, const void* state, void* out128) {
+  memset(out128, 0, 128);
+  KPass h;
+  memcpy(&h, blob, sizeof h);
+  const int tma_min_l = getenv("QS_JIT_TMA_L") ? atoi(getenv("QS_JIT_TMA_L")) : 5;
+  int l = 0;
+  while (l < kChunkBits && h.cpos[l] == l) l++;
+  TPlan tp;
+  if (h.src_mode != 0 || h.kernel == KK_SMALL || l >= tma_min_l || Gen::low_run(h.phases[0]) > 1 ||
+      !tensor_plan(h, &tp))
+    return false;
+  Driver& d = driver();
+  if (!d.tmap) return false;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5], estr[5];
+  for (int k = 0; k < tp.rank; k++) {
+    dims[k] = k == 0 ? (2ull << tp.len[0]) : (1ull << tp.len[k]);
+    box[k] = tp.chunk[k] ? (cuuint32_t)dims[k] : 1u;
+    estr[k] = 1;
+    if (k > 0) strides[k - 1] = (cuuint64_t)16 << tp.pos[k];
+  }
+  return d.tmap((CUtensorMap*)out128, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)tp.rank,
+                const_cast<void*>(state), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 cudaError_t jit_launch(void* fn, int grid, size_t smem, const unsigned char* dblob,
-                       double2* state, u64 rank_base, const u64* vtab, const u64* xpeer8,
-                       const void* pool_host, size_t pool_bytes, cudaStream_t st) {
+                       const unsigned char* hblob, double2* state, u64 rank_base, const u64* vtab,
+                       const u64* xpeer8, const void* pool_host, size_t pool_bytes, cudaStream_t st) {
+  alignas(64) unsigned char tm[128];
+  jit_tensor_map(hblob, state, tm);
   Driver& d = driver();
   int threads = kThreads;
   {
@@ -1448,8 +1540,8 @@ cudaError_t jit_launch(void* fn, int grid, size_t smem, const unsigned char* dbl
   u64 xp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (xpeer8) memcpy(xp, xpeer8, sizeof xp);
   void* args[] = {(void*)&dblob, (void*)&state, (void*)&rank_base, (void*)&vtab, (void*)xp,
-                  (void*)pool_host};
-  if (!pool_bytes) args[5] = nullptr;
+                  (void*)tm, (void*)pool_host};
+  if (!pool_bytes) args[6] = nullptr;
   CUresult r = d.launch((CUfunction)fn, (unsigned)grid, 1, 1, (unsigned)threads, 1, 1, (unsigned)smem,
                         (CUstream)st, args, nullptr);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorLaunchFailure;
