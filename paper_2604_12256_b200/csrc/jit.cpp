@@ -91,9 +91,6 @@ __device__ __forceinline__ double2 cis_tab(u64 t, const double2* __restrict__ T)
 __device__ __forceinline__ int swz(int c) {
   return c ^ (((c >> 3) ^ (c >> 6) ^ (c >> 9) ^ (c >> 12)) & 7);
 }
-__device__ __forceinline__ double2 ld2(const double* p) {
-  return __ldg(reinterpret_cast<const double2*>(p));
-}
 __device__ __forceinline__ u32 sa(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(u64* b, u32 n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(sa(b)), "r"(n) : "memory");
@@ -120,7 +117,6 @@ __device__ __forceinline__ void cp_async_wait_group0() { asm volatile("cp.async.
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(sa(dst)), "l"(src) : "memory");
 }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 // the mbarrier sees one arrival once all of this thread's prior cp.async land
 __device__ __forceinline__ void cp_async_mbar_arrive(u64* b) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(sa(b)) : "memory");
