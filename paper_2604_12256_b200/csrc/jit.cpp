@@ -947,7 +947,7 @@ struct Gen {
     o << "extern \"C\" __global__ void __launch_bounds__(" << nthreads << ", " << (NG == 1 && NB <= 1 ? 2 : 1)
       << ")\n" << kname
       << "(const unsigned char* __restrict__ blob, double2* __restrict__ state, u64 rank_base, "
-         "const u64* __restrict__ vtab, const QsXPeer xp, const __grid_constant__ QsTmap tmap"
+         "const u64* __restrict__ vtab, const QsXPeer xp, const __grid_constant__ QsTmap tensmap"
       << (param_pool ? ", const QsPool P" : "") << ") {\n";
     o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n";
     const size_t buf_bytes = (size_t)NB * CH * 16;
@@ -1006,7 +1006,7 @@ struct Gen {
       o << "  const int tcl0 = " << tc_expr(0) << ";\n";
       o << "  for (u32 k = grp; k < " << NB << "u; k += " << NG << "u)\n"
         << "    if (tid < 32 && " << chunk_of("k") << " < " << N << ") { issue(state, corder(" << chunk_of("k") << ")"
-        << ", bufs + k * " << CH << ", mbar + k, tid, &tmap); if (tid == 0) issued[k] = 1u; }\n";
+        << ", bufs + k * " << CH << ", mbar + k, tid, &tensmap); if (tid == 0) issued[k] = 1u; }\n";
     } else if (pipe) {
       std::string tpd = "(0ull";
       for (int i = 0; i < kLogT; i++)
@@ -1074,7 +1074,7 @@ struct Gen {
     const std::string refill =
         use_tma ? "    gbar(1u + grp);  // every thread is done reading the buffer\n"
                   "    if (tid < 32 && " + nxt + " < " + N +
-                  ") { fence_proxy_async(); issue(state, corder(" + nxt + "), sch, mbar + kb, tid, &tmap); " + count + " }\n"
+                  ") { fence_proxy_async(); issue(state, corder(" + nxt + "), sch, mbar + kb, tid, &tensmap); " + count + " }\n"
                 : "    gbar(1u + grp);  // every thread is done reading the buffer\n"
                   "    if (" + nxt + " < " + N + ") { issue_async(state, corder(" + nxt + "), sch, mbar + kb, tpd, sd); " +
                   count + " }\n";

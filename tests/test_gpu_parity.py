@@ -401,6 +401,7 @@ def test_bench_workloads_30_properties(qs, workload):
     gates = bench.make_circuit(workload, n)
     s = qs.Simulator(n)
     s.apply(gates)
+    assert qs.jit_info(s)["jit_errors"] == 0   # the specialised kernels ran
     assert abs(_norm(s, n) - 1.0) < 1e-10
     rng = np.random.default_rng(3)
     offs = [int(o) for o in rng.integers(0, (1 << n) - 4096, size=6)]

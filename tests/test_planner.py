@@ -246,3 +246,18 @@ def test_fusable_swaps_marked():
     # replay (the fused exchange has the swap's semantics) still matches
     psi = replay(plan, n, ranks)
     assert np.max(np.abs(psi - oracle.apply_circuit(n, gates))) < 1e-11
+
+
+def test_specialised_kernels_compile(tmp_path, monkeypatch):
+    """Every pass shape of the bench workloads compiles as a specialised
+    sm_100a kernel (NVRTC runs without a GPU): a generator bug must fail
+    here, not silently fall back to the interpreter kernels on the GPU."""
+    monkeypatch.setenv("QS_JIT_CACHE", str(tmp_path))
+    import bench
+    cfg = qs.make_config(jit_min_qubits=0)
+    n = 20
+    for w in ("qft", "rzz", "diag", "qaoa", "rand"):
+        gates = bench.make_circuit(w, n)
+        for ranks in (1, 4):
+            qs.plan_json(n, gates, n_ranks=ranks, config=cfg, basis=5, detail=2)
+    assert any(p.suffix == ".cubin" for p in tmp_path.iterdir())
