@@ -119,6 +119,23 @@ def test_flag_combinations(qs, flags):
     assert maxdiff(psi, oracle.apply_circuit(n, gates, x=11)) < TOL
 
 
+def test_tensor_tma_load_pass(qs):
+    """A read pass with a 128 B low run and few position runs (positions
+    0-2 + 9-17): loaded with one cp.async.bulk.tensor per chunk."""
+    n = 20
+    g1 = W.random_circuit(n, 60, 4)
+    g2 = [W.Gate("RX", (q,), (), (0.1 * q,)) for q in range(9, 18)] + [W.Gate("CZ", (13,), (4,))]
+    s = qs.Simulator(n)
+    s.set_config(qs.make_config(jit_min_qubits=0))
+    s.apply(g1)
+    s.apply(g2)
+    psi = s.state()
+    assert qs.jit_info(s)["jit_errors"] == 0
+    s.close()
+    want = oracle.apply_circuit(n, g2, state=oracle.apply_circuit(n, g1))
+    assert maxdiff(psi, want) < TOL
+
+
 def test_not_product_state_second_circuit(qs):
     """Second apply on a non-product state: plain loads (no booster)."""
     n = 16
