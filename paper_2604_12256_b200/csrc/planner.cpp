@@ -932,7 +932,7 @@ int encode_pass(const PassPlan& p, int rank, std::vector<unsigned char>& out, st
   h.x_shift = p.x_j ? p.nl - p.x_j : 0;
   h.x_mask = p.x_j ? (1 << p.x_j) - 1 : 0;
   memset(h.x_pos, 0, sizeof h.x_pos);
-  for (int i = 0; i < p.x_j; i++) h.x_pos[i] = (int8_t)p.x_pos[i];
+  for (int i = 0; i < p.x_j && i < (int)sizeof h.x_pos; i++) h.x_pos[i] = (int8_t)p.x_pos[i];
   int n_hu = 0;
   std::vector<KOp> kops;
   std::vector<KGroup> kgroups;
