@@ -944,7 +944,9 @@ struct Gen {
     // fused swap: destination base per value of the exported
     // top local bits (receive buffers of this rank or its peers, by value)
     o << "struct QsXPeer { u64 v[8]; };\n";
-    o << "extern \"C\" __global__ void __launch_bounds__(" << nthreads << ", " << (NG == 1 && NB <= 1 ? 2 : 1)
+    // QS_JIT_WO_MINB: A/B knob for the resident-CTA target of one-group passes
+    static const int wo_minb = getenv("QS_JIT_WO_MINB") ? atoi(getenv("QS_JIT_WO_MINB")) : 2;
+    o << "extern \"C\" __global__ void __launch_bounds__(" << nthreads << ", " << (NG == 1 && NB <= 1 ? wo_minb : 1)
       << ")\n" << kname
       << "(const unsigned char* __restrict__ blob, double2* __restrict__ state, u64 rank_base, "
          "const u64* __restrict__ vtab, const QsXPeer xp, const __grid_constant__ QsTmap tensmap"
