@@ -682,7 +682,7 @@ int execute(qs_ctx* ctx, const Plan& plan) {
             u64 grid = (u64)num_sms_of(sh.device) * per_sm;
             // with QS_JIT_WO_MINB (A/B knob) keep grids a multiple of 8 so the
             // hoisted expand gathers stay enabled at 3 CTAs per SM
-            if (getenv("QS_JIT_WO_MINB") && per_sm >= 3 && grid > 8) grid &= ~7ull;
+            if (getenv("QS_JIT_WO_MINB") && per_sm != 2 && grid > 8) grid &= ~7ull;
             if (grid > h.n_chunks) grid = h.n_chunks;
             const unsigned char* hb = blobs[si].data() + blob_off[si][k];
             const size_t pb = jit_param_bytes(hb);
