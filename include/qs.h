@@ -149,11 +149,21 @@ int qs_nccl_unique_id(void *id_out_128);
 int qs_create_rank(int n_qubits, int world_size, int rank, int device,
                    const void *nccl_id_128, qs_ctx **out);
 
-void qs_destroy(qs_ctx *ctx); /* frees everything; NULL-safe */
+/* qs_destroy: frees every device/host resource of the handle (state shards,
+ * receive buffers, descriptor arena, sub-state pool, NCCL communicators,
+ * streams, CUDA IPC mappings).  NULL-safe; valid on a poisoned handle.
+ * Owns nothing the caller passed in (gate matrices are borrowed per call). */
+void qs_destroy(qs_ctx *ctx);
 
 /* ---------------------------------------------------------------- config */
-int qs_set_config(qs_ctx *ctx, const qs_config_t *cfg); /* EINVAL if out of range */
+/* qs_set_config: the optimiser environment {C, F, D, B, flags} of Alg. 4
+ * (P:L370-374).  chunk_qubits must be 12 (the 2^12-amplitude, 64 KiB chunk
+ * of this build); fuse_cap in [1, 4] (4 = one 16x16 register op); diag_cap
+ * in [0, 64]; boost_div in [1, 64]; flags within QS_OPT_ALL;
+ * jit_min_qubits >= 0.  QS_EINVAL otherwise (config unchanged). */
+int qs_set_config(qs_ctx *ctx, const qs_config_t *cfg);
 int qs_get_config(const qs_ctx *ctx, qs_config_t *cfg);
+/* Defaults: C = 12, F = 4, D = 0 (no cap), B = 2, all flags, jit 18. */
 void qs_default_config(qs_config_t *cfg);
 
 /* ----------------------------------------------------------------- state */
@@ -174,17 +184,33 @@ int qs_set_basis_state(qs_ctx *ctx, uint64_t x);
 int qs_apply_circuit(qs_ctx *ctx, const qs_gate_t *gates, size_t n_gates);
 
 /*
- * qs_get_state: amplitudes [offset, offset+count) in LOGICAL index order
- * (undoes the virtual qubit map and the sharding) into the caller-owned
- * host buffer `host_out` of 2*count doubles.  Collective in rank mode
- * (every rank receives the slice).  QS_EINVAL if the range exceeds 2^n.
+ * qs_get_state: amplitudes alpha_i, i in [offset, offset+count), of the state
+ * vector |psi> = sum_i alpha_i |i> of Eq. 1 ("two 64-bit
+ * floating-point numbers" each) in LOGICAL index order: qubit q is bit q of
+ * i (reading c1); the virtual qubit map (Eq. 4 reordering) and
+ * the sharding by the top log2(P) qubits are undone on the device (K6).
+ * host_out: caller-owned host buffer of 2*count doubles (re, im interleaved;
+ * pinned memory makes it one DMA).  Collective in rank mode (every rank
+ * receives the slice).  Errors: QS_EINVAL (NULL buffer with count > 0,
+ * range beyond 2^n), QS_EPOISONED, QS_ECUDA/QS_ENCCL (handle poisoned).
  */
 int qs_get_state(qs_ctx *ctx, double *host_out, uint64_t offset, uint64_t count);
 
-/* |a_i|^2 for the same logical slice into `host_out` (count doubles). */
+/*
+ * qs_probabilities: |alpha_i|^2 (Eq. 1: the measurement
+ * probability of basis state |i>) for the same logical slice into the
+ * caller-owned host buffer `host_out` of count doubles.  Same ordering,
+ * collectivity and errors as qs_get_state.
+ */
 int qs_probabilities(qs_ctx *ctx, double *host_out, uint64_t offset, uint64_t count);
 
+/* qs_get_stats: plan and timing statistics of the last qs_apply_circuit
+ * (qs_stats_t above; paper_updates = the "state vector updates" count of
+ * P:L336/L471, t_plan_ms = the optimiser time P:L382 bounds).  QS_EINVAL on
+ * NULL arguments. */
 int qs_get_stats(const qs_ctx *ctx, qs_stats_t *out);
+/* Message of the last failure on the handle (owned by the handle, valid until
+ * the next call on it); "NULL handle" for NULL. */
 const char *qs_last_error(const qs_ctx *ctx);
 
 /* ---------------------------------------------------- plan inspection (host) */
@@ -236,9 +262,12 @@ void *qs_get_stream(const qs_ctx *ctx, int i);
 
 /* Pass specialisation (NVRTC, sm_100a): the chunk/dense/diagonal passes of
  * large shards are compiled per pass structure and cached (QS_JIT=0|1|auto;
- * cache directory QS_JIT_CACHE).  Writes a JSON object {jit_launches,
- * jit_errors, compile_ms, compiles, disk_hits, last_error} (process-wide
- * compile counters; launch counters of this handle) into buf; returns its
+ * cache directory QS_JIT_CACHE; all passes of a call are prepared -- in
+ * parallel -- before its first launch).  Writes a JSON object {jit_launches,
+ * jit_errors, compile_ms, compiles, disk_hits, prep_ms, variants:
+ * {write_only, bulk_tma, tensor_tma, cp_async}, last_error} (process-wide
+ * compile counters; launch counters of this handle, per chunk refill engine;
+ * prep_ms = kernel preparation time of the last call) into buf; returns its
  * length. */
 int64_t qs_jit_info(const qs_ctx *ctx, char *buf, size_t cap);
 /* launches, summed device ms and ALGORITHMIC bytes (32 B per amplitude per

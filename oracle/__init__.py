@@ -49,7 +49,7 @@ def build(force: bool = False) -> str:
     """Compile oracle.c with gcc (-O2 -fopenmp).  Building the checker is not
     using it; __graft_entry__.build() calls this."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        cmd = ["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=gnu11",
+        cmd = ["gcc", "-O2", "-fcx-limited-range", "-fopenmp", "-fPIC", "-shared", "-std=gnu11",
                "-o", _LIB, _SRC, "-lm"]
         subprocess.run(cmd, check=True)
     return _LIB
@@ -77,6 +77,13 @@ def _load():
 
 def num_threads() -> int:
     return _load().oracle_num_threads()
+
+
+def set_num_threads(k: int) -> None:
+    """OpenMP thread count of the oracle's loop (libgomp's process-wide
+    setting; the CPU-baseline single-thread leg)."""
+    _load()
+    ctypes.CDLL("libgomp.so.1").omp_set_num_threads(int(k))
 
 
 def _marshal(gates):
@@ -128,11 +135,16 @@ def basis_state(n: int, x: int = 0) -> np.ndarray:
     return psi
 
 
-def apply_circuit(n: int, gates, state: np.ndarray | None = None, x: int = 0) -> np.ndarray:
-    """Alg. 1 over ``gates`` starting from ``state`` (copied) or |x>."""
+def apply_circuit(n: int, gates, state: np.ndarray | None = None, x: int = 0,
+                  inplace: bool = False) -> np.ndarray:
+    """Alg. 1 over ``gates`` starting from ``state`` (copied, or updated in
+    place with ``inplace=True`` -- large states) or |x>."""
     lib = _load()
     if state is None:
         psi = basis_state(n, x)
+    elif inplace:
+        psi = state
+        assert psi.dtype == np.complex128 and psi.shape == (1 << n,) and psi.flags.c_contiguous
     else:
         psi = np.array(state, dtype=np.complex128, copy=True)
         assert psi.shape == (1 << n,)

@@ -39,6 +39,8 @@ cudaError_t launch_gather(const double2* state, double2* out, u64 off, u64 count
                           const int8_t* dmap, int nl, u64 rank, int probs, cudaStream_t st);
 bool jit_prepare(const unsigned char* blob, int device, void** fn_out, int* grid_per_sm,
                  size_t* smem_out, std::string& err, bool compile_only);
+int jit_prepare_all(const std::vector<const unsigned char*>& blobs, int device,
+                    std::vector<JitPrepared>& out, bool compile_only);
 cudaError_t jit_launch(void* fn, int grid, size_t smem, const unsigned char* dblob,
                        const unsigned char* hblob, double2* state, u64 rank_base, const u64* vtab,
                        const u64* xpeer8, const void* pool_host, size_t pool_bytes, cudaStream_t st);
@@ -47,7 +49,6 @@ cudaError_t launch_shape_table(const unsigned char* dblob, u64* tab, u64 rank_ba
                                const TabCols& v, cudaStream_t st);
 size_t jit_param_bytes(const unsigned char* blob);
 void jit_stats(double* compile_ms, uint64_t* compiles, uint64_t* disk_hits);
-std::string jit_source(const unsigned char* blob);
 }  // namespace qs
 
 namespace {
@@ -130,6 +131,8 @@ struct qs_ctx {
   size_t host_tmp_cap = 0;
   bool timing = true;
   uint64_t jit_launches = 0, jit_errors = 0;
+  uint64_t jit_variant[JV_NUM] = {0, 0, 0, 0};  // launches per refill engine (handle lifetime)
+  double prep_ms = 0;                           // last call: kernel preparation (compile/load)
   std::string jit_last_error;
   // fused swaps: pointer swaps so far (all shards and ranks
   // in lockstep), peer access state (0 unknown, 1 ready, -1 unavailable),
@@ -335,7 +338,7 @@ double2* recv_buffer(qs_ctx* ctx, int d) {
 // index i whose bits at lpos spell s goes to rank dest(r, s), at i with
 // those bits replaced by u(r) -- so the base is that rank's receive buffer
 // + (dep(u(r)) - dep(s)) amplitudes, dep(v) placing bit i of v at lpos[i].
-void fused_targets(qs_ctx* ctx, const Step& st, int r, u64 out[8]) {
+void fused_targets(qs_ctx* ctx, const Step& st, int r, u64 out[1 << kMaxXBits]) {
   const int j = st.j, nl = ctx->nl;
   auto dep = [&](int v) {
     u64 x = 0;
@@ -344,7 +347,7 @@ void fused_targets(qs_ctx* ctx, const Step& st, int r, u64 out[8]) {
   };
   int ur = 0;
   for (int i = 0; i < j; i++) ur |= ((r >> (st.gpos[i] - nl)) & 1) << i;
-  for (int s = 0; s < 8; s++) {
+  for (int s = 0; s < (1 << kMaxXBits); s++) {
     out[s] = 0;
     if (s >= (1 << j)) continue;
     int d = r;
@@ -439,7 +442,17 @@ int exec_swap(qs_ctx* ctx, const Step& st) {
 }
 
 // -------------------------------------------------------------- execute
+int execute_steps(qs_ctx* ctx, const Plan& plan);
+
+// Every error after the first launch leaves a partly applied circuit:
+// the handle is poisoned (include/qs.h, qs_apply_circuit).
 int execute(qs_ctx* ctx, const Plan& plan) {
+  const int rc = execute_steps(ctx, plan);
+  if (rc && ctx->launches) ctx->poisoned = true;
+  return rc;
+}
+
+int execute_steps(qs_ctx* ctx, const Plan& plan) {
   ctx->n_fused_swaps = 0;  // per call (qs_stats_t reports the last call)
   ctx->fused_pending = false;
   // sub-state pool
@@ -509,6 +522,68 @@ int execute(qs_ctx* ctx, const Plan& plan) {
       o += (blobs[si].size() + 255) & ~(size_t)255;
     }
   }
+  // Specialised kernels for every pass are compiled (in parallel) and loaded
+  // before anything launches, so a failure cannot leave a half-applied plan:
+  // a pass whose kernel is not ready runs on the interpreter kernel, and a
+  // swap fused into such a pass runs unfused.
+  const auto tp0 = std::chrono::steady_clock::now();
+  std::vector<std::vector<JitPrepared>> prep(ctx->shards.size(), std::vector<JitPrepared>(plan.steps.size()));
+  std::vector<char> step_jit(plan.steps.size(), 1);  // ready on every shard
+  for (size_t si = 0; si < ctx->shards.size(); si++) {
+    Shard& sh = ctx->shards[si];
+    std::vector<const unsigned char*> list;
+    std::vector<size_t> at;
+    for (size_t k = 0; k < plan.steps.size(); k++) {
+      const Step& st = plan.steps[k];
+      if (st.type != Step::PASS || st.pass.kernel == KK_SMALL || st.pass.nl < ctx->cfg.jit_min_qubits) {
+        step_jit[k] = 0;
+        continue;
+      }
+      list.push_back(blobs[si].data() + blob_off[si][k]);
+      at.push_back(k);
+    }
+    if (list.empty()) continue;
+    CU(cudaSetDevice(sh.device));
+    std::vector<JitPrepared> res;
+    jit_prepare_all(list, sh.device, res, false);
+    for (size_t i = 0; i < at.size(); i++) {
+      if (!res[i].ok) {
+        ctx->jit_errors++;
+        ctx->jit_last_error = res[i].err;
+        step_jit[at[i]] = 0;
+      }
+      prep[si][at[i]] = std::move(res[i]);
+    }
+  }
+  // fused swaps (f1) need the specialised kernel of the exporting pass on
+  // every rank: in rank mode all ranks vote (min) so they agree
+  bool any_fusable = false;
+  for (size_t k = 0; k + 1 < plan.steps.size(); k++)
+    if (plan.steps[k].type == Step::PASS && plan.steps[k].pass.x_j && plan.steps[k + 1].type == Step::SWAP &&
+        plan.steps[k + 1].fusable)
+      any_fusable = true;
+  bool fuse_vote = true;
+  if (any_fusable && ctx->mode == M_RANK && ctx->n_ranks > 1) {
+    double v = 1.0;
+    for (size_t k = 0; k + 1 < plan.steps.size(); k++)
+      if (plan.steps[k].type == Step::PASS && plan.steps[k].pass.x_j && !step_jit[k]) v = 0.0;
+    Shard& sh = ctx->shards[0];
+    CU(cudaSetDevice(sh.device));
+    double* dv = reinterpret_cast<double*>(sh.bar) + 1;
+    CU(cudaMemcpyAsync(dv, &v, sizeof v, cudaMemcpyHostToDevice, sh.stream));
+    NC(ncclAllReduce(dv, dv, 1, ncclDouble, ncclMin, sh.comm, sh.stream));
+    CU(cudaMemcpyAsync(&v, dv, sizeof v, cudaMemcpyDeviceToHost, sh.stream));
+    CU(cudaStreamSynchronize(sh.stream));
+    fuse_vote = v == 1.0;
+  }
+  auto will_fuse = [&](size_t k) {
+    if (k + 1 >= plan.steps.size()) return false;
+    const Step& st = plan.steps[k];
+    const Step& nx = plan.steps[k + 1];
+    return st.type == Step::PASS && st.pass.x_j && nx.type == Step::SWAP && nx.fusable && fuse_vote &&
+           step_jit[k] && ensure_peers(ctx) == 1;
+  };
+  ctx->prep_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count();
   for (Shard& sh : ctx->shards) {
     CU(cudaSetDevice(sh.device));
     sh.timed.clear();
@@ -576,8 +651,8 @@ int execute(qs_ctx* ctx, const Plan& plan) {
     // once every peer is done with all earlier steps (an unfused swap's
     // local copy or a permute may still read the buffer that is now the
     // peer's receive buffer).
-    if (st.type == Step::PASS && st.pass.x_j && k + 1 < plan.steps.size() &&
-        plan.steps[k + 1].type == Step::SWAP && plan.steps[k + 1].fusable && ensure_peers(ctx) == 1) {
+    const bool fuse = will_fuse(k);
+    if (fuse) {
       rc = shard_barrier(ctx);
       if (rc) return rc;
     }
@@ -656,29 +731,21 @@ int execute(qs_ctx* ctx, const Plan& plan) {
           KPass h;
           memcpy(&h, blobs[si].data() + blob_off[si][k], sizeof h);
           double2* buf = (p.buf == 0) ? sh.state : (sh.subpool + sub_off[p.buf]);
-          void* fn = nullptr;
-          int per_sm = 1;
-          size_t smem = 0;
-          std::string jerr;
           // fused swap: this pass exports the next swap's pieces (decided the
-          // same way on every shard and rank: the plan + collective peer setup)
-          u64 xp[8];
-          for (int s = 0; s < 8; s++) xp[s] = (u64)buf;
-          bool fuse = false;
-          if (h.x_mask && k + 1 < plan.steps.size()) {
-            const Step& nx = plan.steps[k + 1];
-            if (nx.type == Step::SWAP && nx.fusable) {
-              if (ensure_peers(ctx) == 1) {
-                fused_targets(ctx, nx, sh.rank, xp);
-                fuse = true;
-                ctx->fused_pending = true;
-              }
-              CU(cudaSetDevice(sh.device));
-            }
+          // same way on every shard and rank: plan, kernel readiness vote,
+          // collective peer setup); otherwise every destination is our own
+          // buffer at our own index
+          u64 xp[1 << kMaxXBits];
+          for (int s = 0; s < (1 << kMaxXBits); s++) xp[s] = (u64)buf;
+          if (fuse) {
+            fused_targets(ctx, plan.steps[k + 1], sh.rank, xp);
+            ctx->fused_pending = true;
           }
-          if (p.kernel != KK_SMALL && p.nl >= ctx->cfg.jit_min_qubits &&
-              jit_prepare(blobs[si].data() + blob_off[si][k], sh.device, &fn, &per_sm, &smem, jerr,
-                          false)) {
+          const JitPrepared& jp = prep[si][k];
+          if (jp.ok) {
+            void* fn = jp.fn;
+            const int per_sm = jp.per_sm;
+            const size_t smem = jp.smem;
             u64 grid = (u64)num_sms_of(sh.device) * per_sm;
             // with QS_JIT_WO_MINB (A/B knob) keep grids a multiple of 8 so the
             // hoisted expand gathers stay enabled at 3 CTAs per SM
@@ -702,18 +769,11 @@ int execute(qs_ctx* ctx, const Plan& plan) {
             CU(jit_launch(fn, (int)grid, smem, dblob, hb, buf, h.rank_base, sh.vtab, xp, hb + h.off_pool,
                           pb, sh.stream));
             ctx->jit_launches++;
+            ctx->jit_variant[jp.variant]++;
           } else {
-            if (!jerr.empty()) ctx->jit_errors++, ctx->jit_last_error = jerr;
+            // interpreter kernel (small passes, jit_min_qubits, or a kernel
+            // that failed to build): stores locally, never fused
             CU(launch_pass(p.kernel, dblob, h, buf, sh.stream));
-            if (fuse && !top_lpos(ctx, plan.steps[k + 1]))
-              return set_err(ctx, QS_EINVAL, "a direct fused swap needs the specialised kernel: " + jerr);
-            if (fuse) {
-              // interpreter kernels store locally: export the pieces by copies
-              const size_t piece = (size_t)1 << h.x_shift;
-              for (int s = 0; s <= h.x_mask; s++)
-                CU(cudaMemcpyAsync((double2*)xp[s] + (size_t)s * piece, buf + (size_t)s * piece,
-                                   piece * sizeof(double2), cudaMemcpyDefault, sh.stream));
-            }
           }
           ctx->launches++;
           kind = (p.buf == 0) ? p.kernel : KK_SUB;  // full-state passes only per kernel
@@ -1106,19 +1166,25 @@ int64_t qs_plan_json(int n_qubits, int n_ranks, const qs_config_t* cfg, int prod
   rc = make_plan(in, ir, plan, err);
   if (rc) return fail(rc);
   // also validate that every pass encodes
+  std::vector<std::vector<unsigned char>> blobs;
   for (const Step& st : plan.steps)
     if (st.type == Step::PASS) {
       std::vector<unsigned char> b;
       rc = encode_pass(st.pass, 0, b, err);
       if (rc) return fail(rc);
-      if (detail >= 2 && st.pass.kernel != KK_SMALL) {
-        // compile the specialised kernel (NVRTC works without a GPU)
-        void* fn = nullptr;
-        int per_sm = 0;
-        size_t smem = 0;
-        if (!jit_prepare(b.data(), 0, &fn, &per_sm, &smem, err, true)) return fail(QS_EINVAL);
-      }
+      if (detail >= 2 && st.pass.kernel != KK_SMALL) blobs.push_back(std::move(b));
     }
+  if (!blobs.empty()) {
+    // compile the specialised kernels (NVRTC works without a GPU), in parallel
+    std::vector<const unsigned char*> list;
+    for (auto& b : blobs) list.push_back(b.data());
+    std::vector<JitPrepared> res;
+    if (jit_prepare_all(list, 0, res, true)) {
+      for (auto& r : res)
+        if (!r.ok) err = r.err;
+      return fail(QS_EINVAL);
+    }
+  }
   std::string js = plan_to_json(plan, detail != 0);
   if (buf && cap) {
     size_t k = std::min(cap - 1, js.size());
@@ -1143,16 +1209,21 @@ int64_t qs_jit_info(const qs_ctx* ctx, char* buf, size_t cap) {
   double ms = 0;
   uint64_t nc = 0, hits = 0;
   jit_stats(&ms, &nc, &hits);
-  char b[512];
+  char b[768];
   std::string last = ctx ? ctx->jit_last_error.substr(0, 200) : "";
   for (char& c : last)
-    if (c == '"' || c == '\\' || c == '\n') c = ' ';
+    if (c == '"' || c == '\\' || c == '\n' || (unsigned char)c < 32) c = ' ';
+  const uint64_t* v = ctx ? ctx->jit_variant : nullptr;
   snprintf(b, sizeof b,
            "{\"jit_launches\":%llu,\"jit_errors\":%llu,\"compile_ms\":%.1f,\"compiles\":%llu,"
-           "\"disk_hits\":%llu,\"last_error\":\"%s\"}",
+           "\"disk_hits\":%llu,\"prep_ms\":%.2f,\"variants\":{\"write_only\":%llu,\"bulk_tma\":%llu,"
+           "\"tensor_tma\":%llu,\"cp_async\":%llu},\"last_error\":\"%s\"}",
            (unsigned long long)(ctx ? ctx->jit_launches : 0),
            (unsigned long long)(ctx ? ctx->jit_errors : 0), ms, (unsigned long long)nc,
-           (unsigned long long)hits, last.c_str());
+           (unsigned long long)hits, ctx ? ctx->prep_ms : 0.0,
+           (unsigned long long)(v ? v[JV_WRITE_ONLY] : 0), (unsigned long long)(v ? v[JV_BULK] : 0),
+           (unsigned long long)(v ? v[JV_TENSOR] : 0), (unsigned long long)(v ? v[JV_CPASYNC] : 0),
+           last.c_str());
   std::string s = b;
   if (buf && cap) {
     size_t k = std::min(cap - 1, s.size());

@@ -27,7 +27,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <atomic>
 #include <map>
+#include <thread>
 #include <mutex>
 #include <sstream>
 #include <string>
@@ -53,6 +55,8 @@ __device__ __forceinline__ double2 cmac(double2 acc, double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, fma(-a.y, b.y, acc.x)),
                       fma(a.x, b.y, fma(a.y, b.x, acc.y)));
 }
+// exp(2 pi i t / 2^64); polynomials: fdlibm's __kernel_sin/__kernel_cos
+// coefficients (see kernels.cu)
 __device__ __forceinline__ double2 cis_turns(u64 t) {
   const u64 q = (t + (1ull << 61)) >> 62;
   const long long f = (long long)(t - (q << 62));
@@ -297,6 +301,8 @@ struct Gen {
   int n_table = 0;          // sincos evaluations left in the loop (need the table)
   bool hoist_capped = false;  // a loop-invariant sincos did not fit in smem
   bool table_free = false;    // generation assumes no table: 4 KB more for hoists
+  bool bad_op = false;        // an op type the generator does not know
+  int variant = 0;            // chunk refill engine (JitVariant)
   // Chunk groups per CTA: multi-layout load passes (compute-heavy between
   // their load and their store) run two groups over three buffers so a load
   // is always in flight; the others run one group (two CTAs per SM, one
@@ -738,6 +744,37 @@ struct Gen {
     o << "  }\n";
   }
 
+  // Wide dense op (OP_DW, 5-6 targets; Eq. 3 generalised) on the
+  // chunk in shared memory: thread t owns base t >> (k-4) and output rows
+  // (t & (2^(k-4)-1))*16 + j; it reads the base's 2^k inputs, accumulates
+  // its 16 rows, and writes them after the group barrier.
+  void wide(const KOp& op) {
+    const int k = op.k, D = 1 << k, g = k - kRegBits;
+    int tm = 0;
+    for (int i = 0; i < k; i++) tm |= 1 << op.tpos[i];
+    o << "    { // wide dense " << k << "q (shared memory)\n";
+    o << "      const u32 wb = tid >> " << g << ", wr = tid & " << ((1 << g) - 1) << "u;\n";
+    o << "      const int cbase = 0";
+    for (int c = 0, bi = 0; c < kChunkBits; c++)
+      if (!(tm >> c & 1)) o << " | (int)(((wb >> " << bi++ << ") & 1u) << " << c << ")";
+    o << ";\n";
+    o << "      const bool wact = ((cphys & " << u(op.ncm) << ") == " << u(op.ncm) << ") && ((cbase & "
+      << op.rcm << ") == " << op.rcm << ");\n";
+    std::string dep = "";
+    for (int i = 0; i < k; i++) dep += " | (((c >> " + std::to_string(i) + ") & 1) << " + std::to_string((int)op.tpos[i]) + ")";
+    o << "      const double* __restrict__ wm = pool + " << op.data << " + 2 * (size_t)(wr * " << kNReg * D << ");\n";
+    for (int j = 0; j < kNReg; j++) o << "      double2 w" << j << " = make_double2(0.0, 0.0);\n";
+    o << "      if (wact) {\n#pragma unroll 2\n        for (int c = 0; c < " << D << "; c++) {\n"
+      << "          const double2 v = sch[swz(cbase" << dep << ")];\n";
+    for (int j = 0; j < kNReg; j++)
+      o << "          w" << j << " = cmac(w" << j << ", __ldg(reinterpret_cast<const double2*>(wm) + " << j * D << " + c), v);\n";
+    o << "        }\n      }\n      gbar(1u + grp);\n      if (wact) {\n";
+    for (int j = 0; j < kNReg; j++) {
+      o << "        { const int c = (int)(wr << 4) + " << j << "; sch[swz(cbase" << dep << ")] = w" << j << "; }\n";
+    }
+    o << "      }\n    }\n";
+  }
+
   void emit_ops(int p, bool diag_only) {
     const KPhase& ph = h.phases[p];
     for (int i = ph.op_begin; i < ph.op_end; i++) {
@@ -756,6 +793,13 @@ struct Gen {
             int b[3], n = 0;
             for (int k = 0; k < kRegBits; k++) if (k != op.sel) b[n++] = k;
             dense(op, p, 3, b);
+          } else if (op.type == OP_D4) {
+            int b[4] = {0, 1, 2, 3};
+            dense(op, p, 4, b);
+          } else if (op.type == OP_DW) {
+            // applied in shared memory at the exchange into this layout
+          } else {
+            bad_op = true;  // never skip an op silently: the pass fails to build
           }
           break;
       }
@@ -886,6 +930,7 @@ struct Gen {
     TPlan tp;
     const bool use_tensor = pipe && l < tma_min_l && low_run(L[0]) <= 1 && tensor_plan(h, &tp);
     const bool use_tma = (pipe && l >= tma_min_l && low_run(L[0]) <= 1 && !getenv("QS_JIT_NOTMA")) || use_tensor;
+    variant = !pipe ? JV_WRITE_ONLY : use_tensor ? JV_TENSOR : use_tma ? JV_BULK : JV_CPASYNC;
     o << "struct __align__(64) QsTmap { u64 v[16]; };\n";
     if (use_tensor) {
       // one tensor copy per chunk (coordinates: the non-chunk runs' index bits)
@@ -1201,6 +1246,10 @@ struct Gen {
         for (int r = 0; r < kNReg; r++)
           o << "    sch[st" << p - 1 << " ^ " << reg_slot(p - 1, r) << "] = " << A(r) << ";\n";
         o << "    gbar(1u + grp);\n";
+        if (p < nph && h.phases[p].op_begin < h.phases[p].op_end && ops[h.phases[p].op_begin].type == OP_DW) {
+          wide(ops[h.phases[p].op_begin]);
+          o << "    gbar(1u + grp);\n";
+        }
         for (int r = 0; r < kNReg; r++)
           o << "    " << A(r) << " = sch[st" << p << " ^ " << reg_slot(p, r) << "];\n";
         if (pipe && p == nlay - 1) o << refill;
@@ -1310,6 +1359,7 @@ struct Compiled {
   int threads = kThreads;
   int blocks_per_sm = 1;
   size_t smem = 0;
+  int variant = 0;
 };
 
 std::mutex g_mu;
@@ -1367,114 +1417,236 @@ const char* jit_kernel_name(int kernel) {
   }
 }
 
-std::string jit_source(const unsigned char* blob, size_t* smem_bytes = nullptr, int* threads = nullptr) {
+namespace {
+struct Source {
+  std::string src, err;
+  u64 hash = 0;
+  size_t smem = 0;
+  int threads = kThreads;
+  int variant = 0;
+  bool ok = false;
+};
+
+Source make_source(const unsigned char* blob) {
+  Source r;
   KPass h;
   memcpy(&h, blob, sizeof h);
   const char* kname = jit_kernel_name(h.kernel);
   const bool multi = h.kernel == KK_CHUNK, diag_only = h.kernel == KK_DIAG;
   Gen g(h, blob);
-  std::string s = g.build(kname, multi, diag_only);
+  r.src = g.build(kname, multi, diag_only);
+  r.smem = g.hz_off + (size_t)g.n_hoist * kThreads * 16;
+  r.threads = g.nthreads;
+  r.variant = g.variant;
+  bool bad = g.bad_op;
   // hoists were capped only by the table's 4 KB: if the extra room takes
   // every loop-invariant sincos out of the loop, no table is needed at all
-  size_t smem = g.hz_off + (size_t)g.n_hoist * kThreads * 16;
-  int nth = g.nthreads;
   if (g.hoist_capped) {
     Gen g2(h, blob);
     g2.table_free = true;
     std::string s2 = g2.build(kname, multi, diag_only);
     if (g2.n_table == 0) {
-      s.swap(s2);
-      smem = g2.hz_off + (size_t)g2.n_hoist * kThreads * 16;
-      nth = g2.nthreads;
+      r.src.swap(s2);
+      r.smem = g2.hz_off + (size_t)g2.n_hoist * kThreads * 16;
+      r.threads = g2.nthreads;
+      r.variant = g2.variant;
+      bad = g2.bad_op;
     }
   }
-  if (smem_bytes) *smem_bytes = smem;
-  if (threads) *threads = nth;
-  return s;
+  if (bad) {
+    r.err = "pass contains an op type the kernel generator does not implement";
+    return r;
+  }
+  r.hash = fnv1a(r.src);
+  r.ok = true;
+  return r;
 }
 
-// Compile (or fetch) the kernel for this pass on `device` (the current
-// device).  Returns false with `err` on failure.
-bool jit_prepare(const unsigned char* blob, int device, void** fn_out, int* grid_per_sm,
-                 size_t* smem_out, std::string& err, bool compile_only) {
-  KPass h;
-  memcpy(&h, blob, sizeof h);
-  const char* kname = jit_kernel_name(h.kernel);
-  size_t smem = 0;
-  int threads = kThreads;
-  const std::string src = jit_source(blob, &smem, &threads);
-  const u64 hash = fnv1a(src);
-  std::lock_guard<std::mutex> lk(g_mu);
-  const u64 key = hash ^ ((u64)(device + 1) * 0x9E3779B97F4A7C15ull);
-  auto it = g_cache.find(key);
-  if (it != g_cache.end() && !compile_only) {
-    *fn_out = (void*)it->second.f;
-    *grid_per_sm = it->second.blocks_per_sm;
-    *smem_out = it->second.smem;
-    return true;
+// Run fn(i) for i in [0, n) on up to QS_JIT_THREADS (default: all host
+// cores, <= 32) threads.
+template <class F>
+void parallel_for(size_t n, F fn) {
+  int nt = (int)std::thread::hardware_concurrency();
+  if (const char* e = getenv("QS_JIT_THREADS")) nt = atoi(e);
+  nt = std::max(1, std::min<int>(nt, 32));
+  if ((size_t)nt > n) nt = (int)n;
+  if (nt <= 1) {
+    for (size_t i = 0; i < n; i++) fn(i);
+    return;
   }
-  char hx[32];
-  snprintf(hx, sizeof hx, "%016llx", (unsigned long long)hash);
-  if (const char* dd = getenv("QS_JIT_DUMP")) {  // debugging: keep the generated source
-    if (FILE* w = fopen((std::string(dd) + "/" + hx + "_" + kname + ".cu").c_str(), "wb")) {
-      fwrite(src.data(), 1, src.size(), w);
-      fclose(w);
+  std::atomic<size_t> next(0);
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; t++)
+    th.emplace_back([&] {
+      for (size_t i; (i = next.fetch_add(1)) < n;) fn(i);
+    });
+  for (auto& x : th) x.join();
+}
+
+bool read_file(const std::string& path, std::vector<char>& out) {
+  FILE* f = fopen(path.c_str(), "rb");
+  if (!f) return false;
+  fseek(f, 0, SEEK_END);
+  long n = ftell(f);
+  fseek(f, 0, SEEK_SET);
+  out.resize(n > 0 ? n : 0);
+  if (n <= 0 || fread(out.data(), 1, n, f) != (size_t)n) out.clear();
+  fclose(f);
+  return !out.empty();
+}
+}  // namespace
+
+std::string jit_source(const unsigned char* blob, size_t* smem_bytes = nullptr, int* threads = nullptr) {
+  Source r = make_source(blob);
+  if (smem_bytes) *smem_bytes = r.smem;
+  if (threads) *threads = r.threads;
+  return r.src;
+}
+
+// Compile (or fetch) the specialised kernels of many passes for `device`
+// (the current device): sources are generated and unique sources compiled
+// in parallel (NVRTC, one program per thread; disk cache first), then the
+// modules are loaded.  compile_only: stop after the cubins (no GPU needed).
+// Returns the number of passes that failed (their JitPrepared.err says why).
+int jit_prepare_all(const std::vector<const unsigned char*>& blobs, int device,
+                    std::vector<JitPrepared>& out, bool compile_only) {
+  const size_t n = blobs.size();
+  out.assign(n, JitPrepared());
+  std::vector<Source> srcs(n);
+  parallel_for(n, [&](size_t i) { srcs[i] = make_source(blobs[i]); });
+  // unique sources that are not loaded on this device yet
+  std::map<u64, size_t> uniq;  // hash -> first pass index
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (size_t i = 0; i < n; i++) {
+      if (!srcs[i].ok) continue;
+      const u64 key = srcs[i].hash ^ ((u64)(device + 1) * 0x9E3779B97F4A7C15ull);
+      if (!compile_only && g_cache.count(key)) continue;
+      uniq.emplace(srcs[i].hash, i);
     }
   }
+  std::vector<std::pair<u64, size_t>> work(uniq.begin(), uniq.end());
+  std::vector<std::vector<char>> cubins(work.size());
+  std::vector<std::string> errs(work.size());
   const std::string dir = cache_dir();
-  const std::string path = dir + "/" + hx + ".cubin";
-  std::vector<char> cubin;
-  FILE* f = fopen(path.c_str(), "rb");
-  if (f) {
-    fseek(f, 0, SEEK_END);
-    long n = ftell(f);
-    fseek(f, 0, SEEK_SET);
-    cubin.resize(n > 0 ? n : 0);
-    if (n <= 0 || fread(cubin.data(), 1, n, f) != (size_t)n) cubin.clear();
-    fclose(f);
-    if (!cubin.empty()) g_disk_hits++;
-  }
-  if (cubin.empty()) {
+  const char* dump = getenv("QS_JIT_DUMP");  // debugging: keep the generated sources
+  parallel_for(work.size(), [&](size_t w) {
+    const Source& S = srcs[work[w].second];
+    char hx[32];
+    snprintf(hx, sizeof hx, "%016llx", (unsigned long long)S.hash);
+    KPass h;
+    memcpy(&h, blobs[work[w].second], sizeof h);
+    const char* kname = jit_kernel_name(h.kernel);
+    if (dump) {
+      if (FILE* f = fopen((std::string(dump) + "/" + hx + "_" + kname + ".cu").c_str(), "wb")) {
+        fwrite(S.src.data(), 1, S.src.size(), f);
+        fclose(f);
+      }
+    }
+    const std::string path = dir + "/" + hx + ".cubin";
+    if (read_file(path, cubins[w])) {
+      std::lock_guard<std::mutex> lk(g_mu);
+      g_disk_hits++;
+      return;
+    }
     auto t0 = std::chrono::steady_clock::now();
-    if (!compile_cubin(src, kname, cubin, err)) return false;
-    g_compile_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    g_compiles++;
+    if (!compile_cubin(S.src, kname, cubins[w], errs[w])) {
+      cubins[w].clear();
+      return;
+    }
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     mkdir(dir.c_str(), 0755);
-    std::string tmp = path + ".tmp" + std::to_string(getpid());
-    FILE* w = fopen(tmp.c_str(), "wb");
-    if (w) {
-      fwrite(cubin.data(), 1, cubin.size(), w);
-      fclose(w);
+    std::string tmp = path + ".tmp" + std::to_string(getpid()) + "_" + std::to_string(w);
+    if (FILE* f = fopen(tmp.c_str(), "wb")) {
+      fwrite(cubins[w].data(), 1, cubins[w].size(), f);
+      fclose(f);
       rename(tmp.c_str(), path.c_str());
     }
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_compile_ms += ms;
+    g_compiles++;
+  });
+  std::map<u64, std::string> failed;  // hash -> error
+  for (size_t w = 0; w < work.size(); w++)
+    if (cubins[w].empty()) failed[work[w].first] = errs[w].empty() ? "compile failed" : errs[w];
+  int bad = 0;
+  if (compile_only) {
+    for (size_t i = 0; i < n; i++) {
+      JitPrepared& P = out[i];
+      P.variant = srcs[i].variant;
+      P.threads = srcs[i].threads;
+      P.smem = srcs[i].smem;
+      if (!srcs[i].ok) P.err = srcs[i].err;
+      else if (failed.count(srcs[i].hash)) P.err = failed[srcs[i].hash];
+      else P.ok = true;
+      bad += !P.ok;
+    }
+    return bad;
   }
-  if (compile_only) return true;
   Driver& d = driver();
-  if (!d.ok) {
-    err = "CUDA driver entry points unavailable";
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (size_t w = 0; w < work.size(); w++) {
+    if (cubins[w].empty()) continue;
+    const Source& S = srcs[work[w].second];
+    const u64 key = S.hash ^ ((u64)(device + 1) * 0x9E3779B97F4A7C15ull);
+    KPass h;
+    memcpy(&h, blobs[work[w].second], sizeof h);
+    const char* kname = jit_kernel_name(h.kernel);
+    CUmodule mod;
+    Compiled c;
+    if (!d.ok) failed[S.hash] = "CUDA driver entry points unavailable";
+    else if (d.load(&mod, cubins[w].data()) != CUDA_SUCCESS) failed[S.hash] = "cuModuleLoadData failed";
+    else if (d.getf(&c.f, mod, kname) != CUDA_SUCCESS) failed[S.hash] = "cuModuleGetFunction failed";
+    else if (S.smem > 48 * 1024 &&
+             d.setattr(c.f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)S.smem) != CUDA_SUCCESS)
+      failed[S.hash] = "shared memory request of " + std::to_string(S.smem) + " B refused";
+    if (failed.count(S.hash)) continue;
+    int nb = 1;
+    if (d.occ(&nb, c.f, S.threads, S.smem) != CUDA_SUCCESS || nb < 1) nb = 1;
+    c.blocks_per_sm = nb;
+    c.smem = S.smem;
+    c.threads = S.threads;
+    c.variant = S.variant;
+    g_cache[key] = c;
+    g_threads[(void*)c.f] = S.threads;
+  }
+  for (size_t i = 0; i < n; i++) {
+    JitPrepared& P = out[i];
+    if (!srcs[i].ok) {
+      P.err = srcs[i].err;
+    } else if (failed.count(srcs[i].hash)) {
+      P.err = failed[srcs[i].hash];
+    } else {
+      const u64 key = srcs[i].hash ^ ((u64)(device + 1) * 0x9E3779B97F4A7C15ull);
+      auto it = g_cache.find(key);
+      if (it == g_cache.end()) {
+        P.err = "internal: kernel missing from the cache";
+      } else {
+        P.ok = true;
+        P.fn = (void*)it->second.f;
+        P.per_sm = it->second.blocks_per_sm;
+        P.smem = it->second.smem;
+        P.threads = it->second.threads;
+        P.variant = it->second.variant;
+      }
+    }
+    bad += !P.ok;
+  }
+  return bad;
+}
+
+// Single-pass form (plan inspection with detail >= 2 compiles one pass).
+bool jit_prepare(const unsigned char* blob, int device, void** fn_out, int* grid_per_sm,
+                 size_t* smem_out, std::string& err, bool compile_only) {
+  std::vector<JitPrepared> r;
+  jit_prepare_all({blob}, device, r, compile_only);
+  if (!r[0].ok) {
+    err = r[0].err;
     return false;
   }
-  CUmodule mod;
-  if (d.load(&mod, cubin.data()) != CUDA_SUCCESS) {
-    err = "cuModuleLoadData failed";
-    return false;
-  }
-  Compiled c;
-  if (d.getf(&c.f, mod, kname) != CUDA_SUCCESS) {
-    err = "cuModuleGetFunction failed";
-    return false;
-  }
-  if (smem > 48 * 1024) d.setattr(c.f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
-  int nb = 1;
-  if (d.occ(&nb, c.f, threads, smem) != CUDA_SUCCESS || nb < 1) nb = 1;
-  c.blocks_per_sm = nb;
-  c.smem = smem;
-  c.threads = threads;
-  g_cache[key] = c;
-  g_threads[(void*)c.f] = threads;
-  *fn_out = (void*)c.f;
-  *grid_per_sm = nb;
-  *smem_out = smem;
+  *fn_out = r[0].fn;
+  *grid_per_sm = r[0].per_sm;
+  *smem_out = r[0].smem;
   return true;
 }
 

@@ -41,8 +41,10 @@ __device__ __forceinline__ double2 cmac(double2 acc, double2 a, double2 b) {
                       fma(a.x, b.y, fma(a.y, b.x, acc.y)));
 }
 
-// exp(2 pi i t / 2^64): quadrant from the top bits (exact), then fdlibm-style
-// kernel polynomials on |x| <= pi/4.
+// exp(2 pi i t / 2^64): quadrant from the top bits (exact), then the
+// minimax kernel polynomials of fdlibm's __kernel_sin / __kernel_cos (Sun
+// Microsystems' freely distributable libm; their published coefficients S1-S6
+// and C1-C6) on |x| <= pi/4.
 __device__ __forceinline__ double2 cis_turns(u64 t) {
   const u64 q = (t + (1ull << 61)) >> 62;
   const long long f = (long long)(t - (q << 62));
@@ -300,6 +302,7 @@ __device__ __forceinline__ void apply_ops(double2 (&a)[kNReg], const KOp* __rest
       op_diag(a, op, groups, shapes, scoef, tid);
       continue;
     }
+    if (op.type == OP_DW) continue;  // applied in shared memory (op_wide)
     if constexpr (!DIAG_ONLY) {
       if (op.type == OP_HU) {
         switch (op.sel) {
@@ -356,11 +359,51 @@ __device__ __forceinline__ void apply_ops(double2 (&a)[kNReg], const KOp* __rest
             default: op_dn<3, 0, 1, 2, 0>(a, m, rcm, tp); break;
           }
           break;
-        default:
+        case OP_D4:
+          op_dn<4, 0, 1, 2, 3>(a, m, rcm, tp);
           break;
+        default:
+          __trap();  // an op this kernel does not know: never skip silently
       }
     }
   }
+}
+
+// Wide dense op (OP_DW, k = 5..6 targets; Eq. 3 generalised) on
+// the chunk staged in shared memory (swizzled slots, chunk index c at
+// swz(c)).  Thread t owns base b = t >> (k-4) (the chunk index with the
+// target bits zero, deposited over the other chunk bits) and the 16 output
+// rows (t & (2^(k-4)-1)) * 16 + j: it reads the 2^k inputs of its base,
+// accumulates its 16 rows, and after a CTA barrier writes them back.
+__device__ void op_wide(double2* sch, const KOp& op, const double* __restrict__ pool, u64 cphys,
+                        uint32_t tid) {
+  const int k = op.k, D = 1 << k, g = k - kRegBits;
+  int tm = 0;
+  for (int i = 0; i < k; i++) tm |= 1 << op.tpos[i];
+  const uint32_t b = tid >> g, rg = tid & ((1u << g) - 1);
+  int cbase = 0, bi = 0;
+  for (int c = 0; c < kChunkBits; c++)
+    if (!(tm >> c & 1)) cbase |= (int)((b >> bi++) & 1u) << c;
+  const bool act = ((cphys & op.ncm) == op.ncm) && ((cbase & (int)op.rcm) == (int)op.rcm);
+  auto dep = [&](int r) {
+    int x = cbase;
+    for (int i = 0; i < k; i++) x |= ((r >> i) & 1) << op.tpos[i];
+    return x;
+  };
+  const double* m = pool + op.data;
+  double2 acc[kNReg];
+#pragma unroll
+  for (int j = 0; j < kNReg; j++) acc[j] = make_double2(0.0, 0.0);
+  if (act)
+    for (int c = 0; c < D; c++) {
+      const double2 v = sch[swz(dep(c))];
+#pragma unroll
+      for (int j = 0; j < kNReg; j++) acc[j] = cmac(acc[j], ldg2(m + 2 * ((size_t)((rg << kRegBits) + j) * D + c)), v);
+    }
+  __syncthreads();
+  if (act)
+#pragma unroll
+    for (int j = 0; j < kNReg; j++) sch[swz(dep((int)(rg << kRegBits) + j))] = acc[j];
 }
 
 // ---------------------------------------------------------- pass kernels
@@ -491,6 +534,20 @@ qs_kpass(const unsigned char* __restrict__ blob, double2* __restrict__ state) {
         for (int r = 0; r < kNReg; r++) sch[swz(L.tc | reg_c(L, r))] = a[r];
         make_layout(P, p, tid, false, L);
         __syncthreads();
+        {
+          const int ob = P.phases[p].op_begin;
+          if (ob < P.phases[p].op_end && __ldg(&ops[ob].type) == OP_DW) {
+            KOp w;
+            w.type = OP_DW;
+            w.k = __ldg(&ops[ob].k);
+            w.rcm = __ldg(&ops[ob].rcm);
+            w.ncm = __ldg(&ops[ob].ncm);
+            w.data = __ldg(&ops[ob].data);
+            for (int i = 0; i < 8; i++) w.tpos[i] = __ldg(&ops[ob].tpos[i]);
+            op_wide(sch, w, pool, cphys, tid);
+            __syncthreads();
+          }
+        }
 #pragma unroll
         for (int r = 0; r < kNReg; r++) a[r] = sch[swz(L.tc | reg_c(L, r))];
       } else {

@@ -20,6 +20,7 @@
 #include <cmath>
 #include <map>
 #include <sstream>
+#include <unordered_set>
 
 #include "planner.hpp"
 
@@ -230,36 +231,80 @@ static void add_diag_op(std::vector<POp>& ops, const IrGate& g, const std::vecto
 }
 
 // GBSA fuse=1: fuse adjacent uncontrolled dense ops when the fused
-// gate's FP64 cost does not exceed the sum of the parts (reading c15).
+// gate's FP64 cost does not exceed the sum of the parts (reading c15).  First
+// the longest run of such ops whose targets fit F (<= 4, the register tile)
+// qubits is tried as one unitary (many small gates on few qubits: e.g. 12
+// two-qubit gates on 4 qubits cost 192 FP64/amp, one 16x16 costs 64); if that
+// does not pay, pairs are fused greedily.
+static std::vector<cd> fuse_pair(const POp& a, const POp& b, std::vector<int>& uni) {
+  uni = a.tpos;
+  for (int p : b.tpos)
+    if (std::find(uni.begin(), uni.end(), p) == uni.end()) uni.push_back(p);
+  std::sort(uni.begin(), uni.end());
+  std::vector<cd> A = embed(a.mat, a.tpos, uni);
+  std::vector<cd> B = embed(b.mat, b.tpos, uni);
+  return matmul(B, A, 1 << (int)uni.size());  // later gate applied after
+}
+
 static void fuse_ops(std::vector<POp>& ops, int fuse_cap) {
   if (fuse_cap < 2) return;
+  const int cap = std::min(fuse_cap, kRegBits);
+  auto fusable = [](const POp& o) { return o.type == POp::DENSE && o.cmask == 0 && (int)o.tpos.size() <= kRegBits; };
   std::vector<POp> out;
-  for (POp& op : ops) {
-    if (!out.empty() && op.type == POp::DENSE && out.back().type == POp::DENSE &&
-        op.cmask == 0 && out.back().cmask == 0) {
-      POp& prev = out.back();
-      std::vector<int> uni = prev.tpos;
-      for (int p : op.tpos)
-        if (std::find(uni.begin(), uni.end(), p) == uni.end()) uni.push_back(p);
-      std::sort(uni.begin(), uni.end());
-      const int ku = (int)uni.size();
-      const double parts = op_cost(prev.mat, prev.is_h) + op_cost(op.mat, op.is_h);
-      if (ku <= std::min(fuse_cap, kRegBits - 1) && dense_cost(ku) / 2 <= parts) {
-        std::vector<cd> A = embed(prev.mat, prev.tpos, uni);
-        std::vector<cd> B = embed(op.mat, op.tpos, uni);
-        std::vector<cd> F = matmul(B, A, 1 << ku);  // later gate applied after
-        if (mat_cost(F) > parts) {
-          out.push_back(std::move(op));
+  for (size_t i = 0; i < ops.size();) {
+    if (fusable(ops[i])) {
+      // longest run from i whose union fits `cap` qubits
+      size_t j = i + 1;
+      u64 um = 0;
+      for (int p : ops[i].tpos) um |= 1ull << p;
+      double parts = op_cost(ops[i].mat, ops[i].is_h);
+      while (j < ops.size() && fusable(ops[j])) {
+        u64 nm = um;
+        for (int p : ops[j].tpos) nm |= 1ull << p;
+        if (popc(nm) > cap) break;
+        um = nm;
+        parts += op_cost(ops[j].mat, ops[j].is_h);
+        j++;
+      }
+      if (j - i >= 3) {
+        POp f = ops[i];
+        for (size_t q = i + 1; q < j; q++) {
+          std::vector<int> uni;
+          f.mat = fuse_pair(f, ops[q], uni);
+          f.tpos = uni;
+          f.n_src += ops[q].n_src;
+        }
+        if (mat_cost(f.mat) <= parts) {
+          f.is_h = f.is_x = false;
+          out.push_back(std::move(f));
+          i = j;
           continue;
         }
-        prev.mat = F;
-        prev.tpos = uni;
-        prev.is_h = prev.is_x = false;
-        prev.n_src += op.n_src;
-        continue;
+      }
+    }
+    POp& op = ops[i];
+    if (!out.empty() && fusable(op) && fusable(out.back())) {
+      POp& prev = out.back();
+      u64 um = 0;
+      for (int p : prev.tpos) um |= 1ull << p;
+      for (int p : op.tpos) um |= 1ull << p;
+      const int ku = popc(um);
+      const double parts = op_cost(prev.mat, prev.is_h) + op_cost(op.mat, op.is_h);
+      if (ku <= cap && dense_cost(ku) / 2 <= parts) {
+        std::vector<int> uni;
+        std::vector<cd> F = fuse_pair(prev, op, uni);
+        if (mat_cost(F) <= parts) {
+          prev.mat = F;
+          prev.tpos = uni;
+          prev.is_h = prev.is_x = false;
+          prev.n_src += op.n_src;
+          i++;
+          continue;
+        }
       }
     }
     out.push_back(std::move(op));
+    i++;
   }
   ops.swap(out);
 }
@@ -333,7 +378,13 @@ static void assign_phases(PassPlan& p) {
   int ph = 0;
   for (size_t i = 0; i < p.ops.size(); i++) {
     const POp& op = p.ops[i];
-    if (op.type == POp::DENSE) {
+    if (op.type == POp::DENSE && (int)op.tpos.size() > kRegBits) {
+      // wide op (5-6 targets): applied to the chunk in shared memory at the
+      // exchange INTO a new layout, so it is the first op of that layout
+      p.phase_regs.push_back(cur);
+      ++ph;
+      cur.clear();
+    } else if (op.type == POp::DENSE) {
       std::vector<int> need;
       for (int pos : op.tpos) need.push_back(cbit(pos));
       std::vector<int> uni = cur;
@@ -492,7 +543,23 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
   const int n_global = nq - nl;
   const bool blocking = (S.cfg->flags & QS_OPT_BLOCK) != 0;
   const int l = 3;  // low positions always in a chunk (128 B runs); 3,4 added when room
-  std::vector<IrGate> rem = std::move(gates);
+  std::vector<IrGate> rem;
+  // A fused diagonal with more distinct monomials than one pass can encode
+  // (kMaxShapes) is split into commuting factors (phase polynomials add).
+  for (IrGate& g : gates) {
+    if (g.type != IrGate::DIAG || g.mono.size() <= (size_t)kMaxShapes || nl <= kSmallMax) {
+      rem.push_back(std::move(g));
+      continue;
+    }
+    merge_mono(g.mono);
+    for (size_t b = 0; b < g.mono.size(); b += kMaxShapes) {
+      IrGate part = g;
+      part.mono.assign(g.mono.begin() + b, g.mono.begin() + std::min(g.mono.size(), b + kMaxShapes));
+      part.n_src = b ? 0 : g.n_src;
+      rem.push_back(std::move(part));
+    }
+  }
+  gates.clear();
   int guard = 0;
   while (!rem.empty()) {
     if (++guard > 1000000) {
@@ -522,7 +589,12 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
     }();
     const double budget = (buf == 0 && S.src_mode && !small) ? wo_budget : 400.0;
     double cost = 0;
-    size_t n_mono = 0;
+    // Encoder limit (kMaxShapes diagonal shapes per pass).  A diagonal op's
+    // shapes are at most its distinct physical masks, and neither the
+    // in-pass monomial sinking nor the fast-path split raises the sum over
+    // ops, so the pass closes before that sum could exceed the limit.
+    size_t shapes_done = 0;            // distinct masks of the earlier diagonal ops
+    std::unordered_set<u64> cur_masks;  // the last diagonal op (open or just closed)
     int dense_taken = 0;
     u64 dense_union = 0;  // dense target positions taken (no-blocking fusion)
     u64 cur_regs = 0;
@@ -544,10 +616,23 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
       }
       if (g.type == IrGate::DIAG) {
         if (s & blocked_nd) { defer(); continue; }
-        if (!small && n_mono + g.mono.size() > 4000 && n_mono > 0) { stop = true; defer(); continue; }
-        if (p.ops.empty() || p.ops.back().type != POp::DIAG) cost += 8;
+        const bool open = !p.ops.empty() && p.ops.back().type == POp::DIAG;
+        if (!small) {
+          std::unordered_set<u64> fresh;
+          for (const Mono& m : g.mono) {
+            const u64 pm = map_mask(m.mask, map);
+            if (!(open && cur_masks.count(pm))) fresh.insert(pm);
+          }
+          const size_t have = shapes_done + cur_masks.size();
+          if (have + fresh.size() > (size_t)kMaxShapes && have > 0) { stop = true; defer(); continue; }
+          if (!open) {
+            shapes_done += cur_masks.size();
+            cur_masks.clear();
+          }
+          cur_masks.insert(fresh.begin(), fresh.end());
+        }
+        if (!open) cost += 8;
         add_diag_op(p.ops, g, map);
-        n_mono += g.mono.size();
         progress = true;
         continue;
       }
@@ -561,10 +646,7 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
       }
       if (global) { defer(); continue; }
       if (!small) {
-        if ((int)g.targets.size() > kRegBits - 1) {
-          err = "dense gates with more than 3 targets need a state of <= 12 local qubits";
-          return QS_EUNSUPPORTED;
-        }
+        const bool wide = (int)g.targets.size() > kRegBits;  // 5-6 targets: shared-memory op
         u64 nn = need | tp;
         if (popc(nn) > kChunkBits) { defer(); continue; }
         const double c = op_cost(g.mat, g.is_h) + 0.5;
@@ -575,7 +657,10 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
           const u64 uni = cur_regs | tp;
           int ph = nphase, cnt = popc(uni);
           u64 nr = uni;
-          if ((tp & ~cur_regs) && cnt > kRegBits) {
+          if (wide) {  // starts a new layout (applied at the exchange into it)
+            ph++;
+            nr = 0;
+          } else if ((tp & ~cur_regs) && cnt > kRegBits) {
             ph++;
             nr = tp;
           }
@@ -689,7 +774,7 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
     // pairs with its own top slot, so that the swap equals "permute the
     // victims to the top, swap, permute back" -- the unfused fallback).
     PassPlan* fuse_into = nullptr;
-    if (buf == 0 && !plan.steps.empty() && plan.steps.back().type == Step::PASS) {
+    if (buf == 0 && j <= kMaxXBits && !plan.steps.empty() && plan.steps.back().type == Step::PASS) {
       PassPlan& lp = plan.steps.back().pass;
       if (lp.buf == 0 && lp.kernel != KK_SMALL && lp.nl >= S.cfg->jit_min_qubits) fuse_into = &lp;
     }
@@ -929,6 +1014,10 @@ int encode_pass(const PassPlan& p, int rank, std::vector<unsigned char>& out, st
     }
   }
   h.scale = 1.0;
+  if (p.x_j < 0 || p.x_j > kMaxXBits) {
+    err = "internal: fused swap exports more than 3 qubits";
+    return QS_EINVAL;
+  }
   h.x_shift = p.x_j ? p.nl - p.x_j : 0;
   h.x_mask = p.x_j ? (1 << p.x_j) - 1 : 0;
   memset(h.x_pos, 0, sizeof h.x_pos);
@@ -1035,7 +1124,39 @@ int encode_pass(const PassPlan& p, int rank, std::vector<unsigned char>& out, st
       };
       KOp k;
       memset(&k, 0, sizeof k);
-      if (op.type == POp::DENSE) {
+      if (op.type == POp::DENSE && (int)op.tpos.size() > kRegBits) {
+        // wide op: chunk-bit targets and controls (shared-memory matvec)
+        if (oi != 0 && p.op_phase[oi - 1] == ph) {
+          err = "internal: wide op is not the first op of its layout";
+          return QS_EINVAL;
+        }
+        if (ph == 0) {
+          err = "internal: wide op in the first layout";
+          return QS_EINVAL;
+        }
+        u64 ncm = 0;
+        uint32_t ccm = 0;
+        for (u64 c = op.cmask; c;) {
+          const int pos = __builtin_ctzll(c);
+          c &= c - 1;
+          const int cb = (pos < p.nl) ? cbit(pos) : m;
+          if (cb < m) ccm |= 1u << cb;
+          else ncm |= 1ull << pos;
+        }
+        k.type = OP_DW;
+        k.k = (uint8_t)op.tpos.size();
+        for (size_t i = 0; i < op.tpos.size(); i++) {
+          const int cb = cbit(op.tpos[i]);
+          if (cb >= m) {
+            err = "internal: wide-op target not in the chunk";
+            return QS_EINVAL;
+          }
+          k.tpos[i] = (int8_t)cb;
+        }
+        k.rcm = ccm;
+        k.ncm = ncm;
+        k.data = put_mat(op.mat);
+      } else if (op.type == POp::DENSE) {
         // controls: register bits -> rho mask; the rest stay physical
         u64 ncm = 0;
         uint32_t rcm = 0;

@@ -6,6 +6,8 @@
 #pragma once
 #include <stdint.h>
 
+#include <string>
+
 namespace qs {
 
 typedef uint64_t u64;
@@ -22,6 +24,7 @@ constexpr int kMaxShapes = 1024;          // diag shapes per pass (smem)
 constexpr int kMaxRuns = 16;              // runs of the chunk-id deposit
 constexpr int kMaxExpand = 4;             // sub-states multiplied by K5
 constexpr int kMaxVaryTab = 64;           // chunk-dependent shapes read from a table
+constexpr int kMaxXBits = 3;              // fused-swap export bits (2^3 destinations)
 
 // Kernel kinds (stats / timing ids).
 enum KernelKind {
@@ -51,6 +54,11 @@ enum OpType : uint8_t {
                 // register subsets (sel = linear mask L), register-pair
                 // terms constant (host table CK16), rcm = touched-rho mask
   OP_HU = 9,    // unnormalised Hadamard (x+y, x-y); pass scale at the store
+  OP_DW = 10,   // wide dense 2^k x 2^k (k = 5, 6) applied to the chunk in
+                // shared memory at the exchange into its layout: k targets =
+                // chunk bits tpos[0..k), chunk-bit control mask rcm, physical
+                // non-chunk control mask ncm, matrix at pool offset data
+                // (row-major, matrix bit i <-> tpos[i]); first op of a layout
   // SMALL kernel ops (physical positions, whole shard in smem)
   OP_SDENSE = 20,
   OP_SDIAG = 21,
@@ -145,6 +153,26 @@ struct TabCols {
   int16_t cis_beg[kMaxTabCis + 1];
   int16_t cis_shape[kMaxTabRefs];
   int32_t width;  // u64 per row: ((n_ang + 1) & ~1) + 2 * n_cis
+};
+
+// Refill engine of a specialised pass (qs_jit_info counts launches per kind).
+enum JitVariant {
+  JV_WRITE_ONLY = 0,  // source fused (booster expand / basis): no loads
+  JV_BULK = 1,        // cp.async.bulk (TMA bulk copies) of >= 512 B runs
+  JV_TENSOR = 2,      // one cp.async.bulk.tensor per chunk
+  JV_CPASYNC = 3,     // per-thread cp.async (128-256 B runs)
+  JV_NUM = 4
+};
+
+// A specialised kernel ready to launch (or why not).
+struct JitPrepared {
+  bool ok = false;
+  void* fn = nullptr;   // CUfunction
+  int per_sm = 1;       // resident CTAs per SM
+  int threads = kThreads;
+  size_t smem = 0;
+  int variant = 0;      // JitVariant
+  std::string err;
 };
 
 }  // namespace qs

@@ -340,13 +340,19 @@ def test_wide_gates_small_state(qs):
     assert maxdiff(psi, oracle.apply_circuit(n, gates, x=9)) < TOL
 
 
-def test_wide_gate_large_state_unsupported(qs):
+def test_wide_gate_large_state(qs):
+    """A 4-target unitary on a 16-qubit state (formerly QS_EUNSUPPORTED) now
+    runs as a register op; 5/6 targets as the shared-memory op (both kernel
+    paths; the full-size cases are in test_gpu_fullsize.py)."""
     rng = np.random.default_rng(2)
-    s = qs.Simulator(16)
-    with pytest.raises(qs.QSError) as e:
-        s.apply([W.Gate("UNITARY", (0, 3, 7, 11), (), (), W.haar_unitary(16, rng))])
-    assert e.value.code == qs.QS_EUNSUPPORTED
-    s.close()
+    n = 16
+    for jit in (0, 99):
+        gates = [W.Gate("UNITARY", (0, 3, 7, 11), (), (), W.haar_unitary(16, rng)),
+                 W.Gate("UNITARY", (1, 2, 5, 9, 14), (4,), (), W.haar_unitary(32, rng)),
+                 W.Gate("UNITARY", (0, 6, 8, 10, 12, 15), (), (), W.haar_unitary(64, rng))]
+        gates = W.random_circuit(n, 30, 5) + gates + W.random_circuit(n, 30, 6)
+        psi, _ = sim_run(qs, n, gates, basis=5, jit_min_qubits=jit)
+        assert maxdiff(psi, oracle.apply_circuit(n, gates, x=5)) < TOL
 
 
 @pytest.mark.parametrize("n", [12, 13])

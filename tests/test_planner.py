@@ -261,3 +261,81 @@ def test_specialised_kernels_compile(tmp_path, monkeypatch):
         for ranks in (1, 4):
             qs.plan_json(n, gates, n_ranks=ranks, config=cfg, basis=5, detail=2)
     assert any(p.suffix == ".cubin" for p in tmp_path.iterdir())
+
+
+# ------------------------------------------------------------ round-2 limits
+
+def test_fused_swaps_capped_at_three_exported_bits():
+    """A fused swap's pass stores to at most 2^3 destinations (the kernel's
+    peer table): with 16 and 32 ranks, swaps of j > 3 qubits stay unfused,
+    and the replay still equals the oracle."""
+    n = 14
+    gates = W.qaoa_maxcut(n, 2, 4)
+    for ranks in (16, 32):
+        nl = n - (ranks.bit_length() - 1)
+        if nl < ranks.bit_length() - 1:
+            continue
+        plan = qs.plan_json(n, gates, n_ranks=ranks, config=qs.make_config(jit_min_qubits=0), detail=True)
+        for i, s in enumerate(plan["steps"]):
+            if s["type"] == "swap" and s["fusable"]:
+                assert s["j"] <= 3
+            if s["type"] == "pass":
+                assert s["x_j"] <= 3
+        psi = replay(plan, n, ranks)
+        assert np.max(np.abs(psi - oracle.apply_circuit(n, gates))) < 1e-11
+    plan = qs.plan_json(24, W.qaoa_maxcut(24, 2, 4), n_ranks=16, config=qs.make_config(jit_min_qubits=0))
+    assert all(s["j"] <= 3 for s in plan["steps"] if s["type"] == "swap" and s["fusable"])
+
+
+def test_many_wide_diagonals_plan_within_encoder_limits():
+    """600 random 6-target DIAGONAL gates on 16 qubits (up to 63 monomials
+    each): the scheduler closes passes before the encoder's shape limit, so
+    the plan encodes, compiles and replays to the oracle."""
+    rng = np.random.default_rng(600)
+    n = 16
+    gates = [W.Gate("DIAGONAL", tuple(int(q) for q in rng.permutation(n)[:6]), (), (),
+                    W.random_phases(64, rng)) for _ in range(600)]
+    plan, psi = run(n, gates, basis=0)
+    assert plan["stats"]["n_passes"] >= 2
+    want = oracle.apply_circuit(n, gates)
+    assert np.max(np.abs(psi - want)) < 1e-11
+
+
+@pytest.mark.parametrize("k", [4, 5, 6])
+def test_wide_unitaries_large_state_plan(k, tmp_path, monkeypatch):
+    """k-target unitaries (Eq. 3 generalised) on a 20-qubit
+    shard: 4 targets become a register op (OP_D4), 5-6 a shared-memory op
+    (OP_DW) at a layout exchange; the plan replays to the oracle and every
+    pass compiles as a specialised kernel."""
+    monkeypatch.setenv("QS_JIT_CACHE", str(tmp_path))
+    rng = np.random.default_rng(40 + k)
+    n = 20
+    gates = W.random_circuit(n, 40, k, diag_bias=0.3, max_generic=3)
+    for _ in range(3):
+        tg = tuple(int(q) for q in rng.permutation(n)[:k])
+        ctl = (int(rng.choice([q for q in range(n) if q not in tg])),) if rng.uniform() < 0.5 else ()
+        gates.append(W.Gate("UNITARY", tg, ctl, (), W.haar_unitary(1 << k, rng)))
+        gates += W.random_circuit(n, 10, int(rng.integers(1000)), diag_bias=0.5)
+    plan = qs.plan_json(n, gates, config=qs.make_config(jit_min_qubits=0), product_state=True, basis=3,
+                        detail=2)
+    check_structure(plan, n, 1)
+    psi = replay(plan, n, 1)
+    assert np.max(np.abs(psi - oracle.apply_circuit(n, gates, x=3))) < 1e-11
+    tks = [len(o["tpos"]) for s in plan["steps"] if s["type"] == "pass" for o in s["ops"] if o["t"] == "dense"]
+    assert max(tks) == k
+
+
+def test_fusion_reaches_four_targets():
+    """fuse_cap = 4 is effective: enough 1-/2-qubit gates on 4 qubits fuse
+    into one 16x16 unitary when the FP64 cost model says it saves work."""
+    rng = np.random.default_rng(7)
+    n = 16
+    qb = [3, 5, 8, 12]
+    gates = []
+    for _ in range(12):
+        a, b = (int(x) for x in rng.choice(qb, 2, replace=False))
+        gates.append(W.Gate("UNITARY", (a, b), (), (), W.haar_unitary(4, rng)))
+    plan, psi = run(n, gates, basis=1)
+    tks = [len(o["tpos"]) for s in plan["steps"] if s["type"] == "pass" for o in s["ops"] if o["t"] == "dense"]
+    assert 4 in tks
+    assert np.max(np.abs(psi - oracle.apply_circuit(n, gates, x=1))) < 1e-11
