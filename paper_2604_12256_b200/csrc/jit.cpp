@@ -286,6 +286,33 @@ struct Gen {
   std::string pv(int off) const {
     return (param_pool ? "P.v[" : "pool[") + std::to_string(off) + "]";
   }
+  // The CK register-pair phase tables of fast diagonals live in a per-CTA
+  // shared-memory copy (cks[], filled once): as loop-invariant parameter
+  // loads the compiler hoists them into registers, which spills the
+  // 16-amplitude register tile (QFT-30 write-only pass: 88 B of spills,
+  // none with the table in shared memory).
+  std::map<int, int> ck_slot;  // complex pool offset (doubles) -> cks index
+  bool ck_smem = false;        // single-layout passes (multi-layout ones keep
+                               // constant-bank operands: no spills there, and
+                               // the extra loads would cost registers)
+  std::string ckv(int off) {
+    if (!ck_smem) return "make_double2(" + pv(off) + ", " + pv(off + 1) + ")";
+    auto it = ck_slot.find(off);
+    int k;
+    if (it == ck_slot.end()) {
+      k = (int)ck_slot.size();
+      ck_slot[off] = k;
+    } else {
+      k = it->second;
+    }
+    return "cks[" + std::to_string(k) + "]";
+  }
+  int n_ck_entries() const {  // upper bound, before generation
+    int c = 0;
+    for (int i = 0; i < h.n_ops; i++)
+      if (ops[i].type == OP_DIAGF && groups[ops[i].data].ck_off >= 0) c += kNReg;
+    return c;
+  }
   // loop-invariant per-thread values hoisted out of the chunk loop
   std::ostringstream pre;
   int n_hoist = 0;
@@ -638,8 +665,7 @@ struct Gen {
         for (int r = 0; r < kNReg; r++) {
           if (!(op.rcm >> r & 1) || (r & L) != s) continue;
           const bool ck = G.ck_off >= 0;
-          const std::string c =
-              ck ? "make_double2(" + pv(G.ck_off + 2 * r) + ", " + pv(G.ck_off + 2 * r + 1) + ")" : "";
+          const std::string c = ck ? ckv(G.ck_off + 2 * r) : "";
           if (fid && !ck) continue;
           if (fid) o << "    " << A(r) << " = cmul(" << A(r) << ", " << c << ");\n";
           else if (!ck) o << "    " << A(r) << " = cmul(" << A(r) << ", F);\n";
@@ -655,8 +681,7 @@ struct Gen {
       if (hc) f.push_back("E0");
       for (int k = 0; k < kRegBits; k++)
         if ((L >> k & 1) && (r >> k & 1)) f.push_back("E" + std::to_string(k + 1));
-      if (G.ck_off >= 0)
-        f.push_back("make_double2(" + pv(G.ck_off + 2 * r) + ", " + pv(G.ck_off + 2 * r + 1) + ")");
+      if (G.ck_off >= 0) f.push_back(ckv(G.ck_off + 2 * r));
       if (f.empty()) continue;
       std::string g = f[0];
       for (size_t i = 1; i < f.size(); i++) g = "cmul(" + g + ", " + f[i] + ")";
@@ -710,8 +735,7 @@ struct Gen {
         else f = "cmul(" + Q + ", " + P[sl] + ")";
         for (int r = 0; r < kNReg; r++) {
           if (!(op.rcm >> r & 1) || (r & L) != s) continue;
-          const std::string c =
-              ck ? "make_double2(" + pv(G.ck_off + 2 * r) + ", " + pv(G.ck_off + 2 * r + 1) + ")" : "";
+          const std::string c = ck ? ckv(G.ck_off + 2 * r) : "";
           if (f.empty() && !ck) continue;
           if (f.empty()) o << "      " << A(r) << " = cmul(" << A(r) << ", " << c << ");\n";
           else if (!ck) o << "      " << A(r) << " = cmul(" << A(r) << ", " << f << ");\n";
@@ -793,9 +817,6 @@ struct Gen {
             int b[3], n = 0;
             for (int k = 0; k < kRegBits; k++) if (k != op.sel) b[n++] = k;
             dense(op, p, 3, b);
-          } else if (op.type == OP_D4) {
-            int b[4] = {0, 1, 2, 3};
-            dense(op, p, 4, b);
           } else if (op.type == OP_DW) {
             // applied in shared memory at the exchange into this layout
           } else {
@@ -815,6 +836,7 @@ struct Gen {
     if (extra_store) L.push_back(default_layout());
     const int nlay = (int)L.size();
     const bool xchg = nlay > 1;  // any shared-memory exchange
+    ck_smem = !xchg;
     const int nsh = h.n_shapes;
     std::vector<int> vary, cons;
     for (int j = 0; j < nsh; j++) {
@@ -1024,7 +1046,8 @@ struct Gen {
     // fill what shared memory is left: 227 KB per CTA (two CTAs per SM: half
     // of 228 KB, less the per-CTA reservation), minus the 4 KB sincos table
     // unless no sincos is left inside the loop (second generation pass)
-    const long smem_cap = ((NG == 1 && NB <= 1) ? 113 * 1024 : 227 * 1024) - (table_free ? 0 : 4096);
+    const long smem_cap = ((NG == 1 && NB <= 1) ? 113 * 1024 : 227 * 1024) - (table_free ? 0 : 4096) -
+                          (ck_smem ? 16l * n_ck_entries() : 0l);
     max_hoist = (int)std::max<long>(0, (smem_cap - (long)hz_off) / (kThreads * 16));
     if (max_hoist > 24) max_hoist = 24;
     if (const char* e = getenv("QS_JIT_MAXHOIST")) max_hoist = std::min(max_hoist, atoi(e));  // experiments
@@ -1298,6 +1321,14 @@ struct Gen {
     o << "}\n";
     std::string s = o.str();
     if (n_hoist) s.insert(loop_pos, "  if (grp == 0) {\n" + pre.str() + "  }\n  __syncthreads();\n");
+    if (!ck_slot.empty()) {
+      std::string t = "  __shared__ double2 cks[" + std::to_string(ck_slot.size()) + "];\n  {\n";
+      for (auto& kv : ck_slot)
+        t += "    if (threadIdx.x == " + std::to_string(kv.second % nthreads) + "u) cks[" + std::to_string(kv.second) +
+             "] = __ldg(reinterpret_cast<const double2*>(pool) + " + std::to_string(kv.first / 2) + ");\n";
+      t += "  }\n";
+      s.insert(ctab_pos, t);
+    }
     if (n_table)
       s.insert(ctab_pos, "  __shared__ double2 ctab[256];\n  for (int i = (int)threadIdx.x; i < 256; i += " +
                              std::to_string(nthreads) + ") ctab[i] = cis_turns((u64)i << 56);\n");

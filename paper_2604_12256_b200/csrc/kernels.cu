@@ -359,9 +359,6 @@ __device__ __forceinline__ void apply_ops(double2 (&a)[kNReg], const KOp* __rest
             default: op_dn<3, 0, 1, 2, 0>(a, m, rcm, tp); break;
           }
           break;
-        case OP_D4:
-          op_dn<4, 0, 1, 2, 3>(a, m, rcm, tp);
-          break;
         default:
           __trap();  // an op this kernel does not know: never skip silently
       }

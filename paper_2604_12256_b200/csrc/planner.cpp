@@ -232,10 +232,11 @@ static void add_diag_op(std::vector<POp>& ops, const IrGate& g, const std::vecto
 
 // GBSA fuse=1: fuse adjacent uncontrolled dense ops when the fused
 // gate's FP64 cost does not exceed the sum of the parts (reading c15).  First
-// the longest run of such ops whose targets fit F (<= 4, the register tile)
-// qubits is tried as one unitary (many small gates on few qubits: e.g. 12
-// two-qubit gates on 4 qubits cost 192 FP64/amp, one 16x16 costs 64); if that
-// does not pay, pairs are fused greedily.
+// the longest run of such ops whose targets fit F (<= 4) qubits is tried as
+// one unitary (many small gates on few qubits: e.g. 12 two-qubit gates on 4
+// qubits cost 192 FP64/amp, one 16x16 costs 64); a 4-qubit result runs as a
+// shared-memory op (two more chunk exchanges), so it must at least halve the
+// cost.  Otherwise pairs are fused greedily up to 3 qubits (register ops).
 static std::vector<cd> fuse_pair(const POp& a, const POp& b, std::vector<int>& uni) {
   uni = a.tpos;
   for (int p : b.tpos)
@@ -248,8 +249,9 @@ static std::vector<cd> fuse_pair(const POp& a, const POp& b, std::vector<int>& u
 
 static void fuse_ops(std::vector<POp>& ops, int fuse_cap) {
   if (fuse_cap < 2) return;
-  const int cap = std::min(fuse_cap, kRegBits);
-  auto fusable = [](const POp& o) { return o.type == POp::DENSE && o.cmask == 0 && (int)o.tpos.size() <= kRegBits; };
+  const int cap = std::min(fuse_cap, kRegBits);          // run fusion
+  const int pcap = std::min(fuse_cap, kRegBits - 1);     // pairwise (register ops)
+  auto fusable = [](const POp& o) { return o.type == POp::DENSE && o.cmask == 0 && (int)o.tpos.size() < kRegBits; };
   std::vector<POp> out;
   for (size_t i = 0; i < ops.size();) {
     if (fusable(ops[i])) {
@@ -274,7 +276,7 @@ static void fuse_ops(std::vector<POp>& ops, int fuse_cap) {
           f.tpos = uni;
           f.n_src += ops[q].n_src;
         }
-        if (mat_cost(f.mat) <= parts) {
+        if (mat_cost(f.mat) * (f.tpos.size() >= (size_t)kRegBits ? 2.0 : 1.0) <= parts) {
           f.is_h = f.is_x = false;
           out.push_back(std::move(f));
           i = j;
@@ -290,7 +292,7 @@ static void fuse_ops(std::vector<POp>& ops, int fuse_cap) {
       for (int p : op.tpos) um |= 1ull << p;
       const int ku = popc(um);
       const double parts = op_cost(prev.mat, prev.is_h) + op_cost(op.mat, op.is_h);
-      if (ku <= cap && dense_cost(ku) / 2 <= parts) {
+      if (ku <= pcap && dense_cost(ku) / 2 <= parts) {
         std::vector<int> uni;
         std::vector<cd> F = fuse_pair(prev, op, uni);
         if (mat_cost(F) <= parts) {
@@ -378,8 +380,8 @@ static void assign_phases(PassPlan& p) {
   int ph = 0;
   for (size_t i = 0; i < p.ops.size(); i++) {
     const POp& op = p.ops[i];
-    if (op.type == POp::DENSE && (int)op.tpos.size() > kRegBits) {
-      // wide op (5-6 targets): applied to the chunk in shared memory at the
+    if (op.type == POp::DENSE && (int)op.tpos.size() >= kRegBits) {
+      // wide op (4-6 targets): applied to the chunk in shared memory at the
       // exchange INTO a new layout, so it is the first op of that layout
       p.phase_regs.push_back(cur);
       ++ph;
@@ -646,7 +648,7 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
       }
       if (global) { defer(); continue; }
       if (!small) {
-        const bool wide = (int)g.targets.size() > kRegBits;  // 5-6 targets: shared-memory op
+        const bool wide = (int)g.targets.size() >= kRegBits;  // 4-6 targets: shared-memory op
         u64 nn = need | tp;
         if (popc(nn) > kChunkBits) { defer(); continue; }
         const double c = op_cost(g.mat, g.is_h) + 0.5;
@@ -1124,8 +1126,10 @@ int encode_pass(const PassPlan& p, int rank, std::vector<unsigned char>& out, st
       };
       KOp k;
       memset(&k, 0, sizeof k);
-      if (op.type == POp::DENSE && (int)op.tpos.size() > kRegBits) {
-        // wide op: chunk-bit targets and controls (shared-memory matvec)
+      if (op.type == POp::DENSE && (int)op.tpos.size() >= kRegBits) {
+        // wide op: chunk-bit targets and controls (shared-memory matvec; a
+        // 16x16 in registers would hold 16 inputs + 16 outputs = all 128
+        // registers of a 2-CTA/SM thread and spill)
         if (oi != 0 && p.op_phase[oi - 1] == ph) {
           err = "internal: wide op is not the first op of its layout";
           return QS_EINVAL;
@@ -1214,9 +1218,6 @@ int encode_pass(const PassPlan& p, int rank, std::vector<unsigned char>& out, st
           int missing = 0;
           while (std::find(sorted.begin(), sorted.end(), missing) != sorted.end()) missing++;
           k.sel = (uint8_t)missing;
-          k.data = put_mat(pm);
-        } else if (t == 4) {
-          k.type = OP_D4;
           k.data = put_mat(pm);
         } else {
           err = "internal: dense op too wide";

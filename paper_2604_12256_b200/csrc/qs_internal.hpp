@@ -46,7 +46,8 @@ enum OpType : uint8_t {
   OP_D1 = 1,    // dense 2x2 on register bit `sel`
   OP_D2 = 2,    // dense 4x4 on register-bit pair `sel` (pair code)
   OP_D3 = 3,    // dense 8x8 on register bits {0..3} \ {sel}
-  OP_D4 = 4,    // dense 16x16 on all register bits
+  // (4: unused -- 4-target ops run as OP_DW: a 16x16 in registers needs
+  //  16 inputs + 16 outputs live, all 128 registers of a thread)
   OP_H = 5,     // Hadamard on register bit `sel`
   OP_X = 6,     // Pauli X on register bit `sel` (register swap)
   OP_DIAG = 7,  // phase polynomial group `data`, general path (2^a sincos)
@@ -54,7 +55,7 @@ enum OpType : uint8_t {
                 // register subsets (sel = linear mask L), register-pair
                 // terms constant (host table CK16), rcm = touched-rho mask
   OP_HU = 9,    // unnormalised Hadamard (x+y, x-y); pass scale at the store
-  OP_DW = 10,   // wide dense 2^k x 2^k (k = 5, 6) applied to the chunk in
+  OP_DW = 10,   // wide dense 2^k x 2^k (k = 4..6) applied to the chunk in
                 // shared memory at the exchange into its layout: k targets =
                 // chunk bits tpos[0..k), chunk-bit control mask rcm, physical
                 // non-chunk control mask ncm, matrix at pool offset data

@@ -131,8 +131,8 @@ def test_second_circuit_read_passes_n23(qs):
 @pytest.mark.parametrize("k", [4, 5, 6])
 def test_wide_unitaries_n22(qs, k):
     """a8 at F = 4 and 4-6-target generic unitaries on a 22-qubit shard
-    (Eq. 3 generalised): k = 4 as a register op, 5-6 as a
-    shared-memory op at a layout exchange; with and without a control."""
+    (Eq. 3 generalised): a shared-memory op at a layout
+    exchange (OP_DW); with and without a control."""
     rng = np.random.default_rng(220 + k)
     n = 22
     gates = W.random_circuit(n, 30, k, diag_bias=0.3)
@@ -147,7 +147,7 @@ def test_wide_unitaries_n22(qs, k):
 
 def test_fused_four_qubit_unitary_n22(qs):
     """fuse_cap = 4 effective: many two-qubit gates on 4 qubits fuse into one
-    16x16 register op; parity with the oracle."""
+    16x16 unitary (shared-memory op); parity with the oracle."""
     rng = np.random.default_rng(5)
     n = 22
     qb = [1, 9, 14, 20]

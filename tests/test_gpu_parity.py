@@ -341,9 +341,9 @@ def test_wide_gates_small_state(qs):
 
 
 def test_wide_gate_large_state(qs):
-    """A 4-target unitary on a 16-qubit state (formerly QS_EUNSUPPORTED) now
-    runs as a register op; 5/6 targets as the shared-memory op (both kernel
-    paths; the full-size cases are in test_gpu_fullsize.py)."""
+    """4-6-target unitaries on a 16-qubit state (formerly QS_EUNSUPPORTED)
+    run as the shared-memory op (OP_DW) on both kernel paths; the full-size
+    cases are in test_gpu_fullsize.py."""
     rng = np.random.default_rng(2)
     n = 16
     for jit in (0, 99):

@@ -304,8 +304,8 @@ def test_many_wide_diagonals_plan_within_encoder_limits():
 @pytest.mark.parametrize("k", [4, 5, 6])
 def test_wide_unitaries_large_state_plan(k, tmp_path, monkeypatch):
     """k-target unitaries (Eq. 3 generalised) on a 20-qubit
-    shard: 4 targets become a register op (OP_D4), 5-6 a shared-memory op
-    (OP_DW) at a layout exchange; the plan replays to the oracle and every
+    shard: 4-6 targets run as a shared-memory op (OP_DW)
+    at a layout exchange; the plan replays to the oracle and every
     pass compiles as a specialised kernel."""
     monkeypatch.setenv("QS_JIT_CACHE", str(tmp_path))
     rng = np.random.default_rng(40 + k)
