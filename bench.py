@@ -348,7 +348,7 @@ def main():
         plan_ms += st["t_plan_ms"]
         dev_ms += st["t_device_ms"]
         for k in ("K1_chunk", "K2_dense", "K3_diag", "small", "K5_expand", "K5_merge", "init", "K4_swap",
-                  "substate"):
+                  "substate", "fused_swap_pass"):
             t = sim.kernel_timing(k)
             a = kt.setdefault(k, {"launches": 0, "ms": 0.0, "bytes": 0})
             for f in a:
@@ -370,15 +370,26 @@ def main():
     # that pass), so only unfused swaps have an exchange time of their own
     nvl = None
     if world > 1 and st["n_swaps"]:
-        sw = kt.get("K4_swap", {"ms": 0.0})
+        sw = kt.get("K4_swap", {"ms": 0.0, "launches": 0})
+        fp = kt.get("fused_swap_pass", {"ms": 0.0, "launches": 0})
         unf = st["n_swaps"] - st["n_fused_swaps"]
+        per_swap = st["bytes_nvlink"] / st["n_swaps"]   # (1 - 2^-j) x shard bytes per swap (equal j here)
         nvl = {"bytes_per_gpu_per_step": st["bytes_nvlink"], "swaps": st["n_swaps"],
                "fused_swaps": st["n_fused_swaps"], "swap_step_ms": sw["ms"] / args.steps,
                "peak_gbs_per_direction": 900.0,
-               "note": "fused swaps: exchange overlapped with the pass (peer stores); swap_step_ms is "
-                       "then only the barrier" if unf == 0 else "NCCL grouped send/recv"}
-        if unf == st["n_swaps"] and sw["ms"] > 0:
-            nvl["achieved_gbs"] = st["bytes_nvlink"] / (sw["ms"] / args.steps * 1e-3) / 1e9
+               "peak_source": "NVLink 5 spec, per direction per GPU (PAPER.md L709 quotes 900 GB/s NVSwitch "
+                              "for the DGX-H100; no measured NVLink peak on file)"}
+        if st["n_fused_swaps"] and fp["ms"] > 0:
+            # the fused pass moves its exported pieces over NVLink while it
+            # streams the shard through HBM: the transfer time is at most the
+            # pass time, so bytes / pass time is a LOWER bound of its NVLink rate
+            b = per_swap * st["n_fused_swaps"]
+            t = fp["ms"] / args.steps * 1e-3
+            nvl["fused"] = {"nvlink_bytes_per_step": b, "pass_ms_per_step": t * 1e3,
+                            "achieved_gbs_lower_bound": b / t / 1e9, "frac_of_900": b / t / 1e9 / 900.0,
+                            "hbm_gbs_of_the_passes": fp["bytes"] / args.steps / t / 1e9}
+        if unf and sw["ms"] > 0 and unf == st["n_swaps"]:
+            nvl["nccl"] = {"achieved_gbs": st["bytes_nvlink"] / (sw["ms"] / args.steps * 1e-3) / 1e9}
 
     # dominant kernel (largest device time) -> roofline
     dom = max(kt.items(), key=lambda kv: kv[1]["ms"])

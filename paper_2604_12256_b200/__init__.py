@@ -37,7 +37,8 @@ KINDS = {
     "SX": 19, "SY": 20, "SW": 21, "UNITARY": 22, "DIAGONAL": 23,
 }
 KERNELS = {"K1_chunk": 0, "K2_dense": 1, "K3_diag": 2, "small": 3, "K5_expand": 4,
-           "K5_merge": 5, "init": 6, "K4_swap": 7, "K6_read": 8, "substate": 9}
+           "K5_merge": 5, "init": 6, "K4_swap": 7, "K6_read": 8, "substate": 9,
+           "fused_swap_pass": 10}
 
 
 class QSError(RuntimeError):

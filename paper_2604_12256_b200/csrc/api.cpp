@@ -776,7 +776,7 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
             CU(launch_pass(p.kernel, dblob, h, buf, sh.stream));
           }
           ctx->launches++;
-          kind = (p.buf == 0) ? p.kernel : KK_SUB;  // full-state passes only per kernel
+          kind = (p.buf != 0) ? KK_SUB : fuse ? KK_XPASS : p.kernel;  // full-state passes only per kernel
           bytes = ((p.src_mode ? 16ull : 32ull) << p.nl);
           break;
         }

@@ -38,7 +38,9 @@ enum KernelKind {
   KK_SWAP = 7,    // K4 exchange (NCCL / copies)
   KK_READ = 8,    // K6 readout gather
   KK_SUB = 9,     // passes on booster sub-states (timing class only)
-  KK_NUM = 10
+  KK_XPASS = 10,  // full-state pass that also performs the next swap's
+                  // exchange by NVLink peer stores (f1; timing class only)
+  KK_NUM = 11
 };
 
 // Register-op types inside a pass.
