@@ -1004,6 +1004,22 @@ struct Gen {
     // their layout exchanges.
     const int NG = groups_per_cta(pipe, nlay);
     const int NB = pipe ? (NG == 1 ? 1 : NG + 1) : (xchg ? NG : 0);
+    // L2 prefetch distance (chunks of the CTA's sequence beyond the
+    // shared-memory ring): cp.async.bulk.prefetch.L2 of chunk k + NB + PF
+    // when chunk k's buffer is refilled, so DRAM latency overlaps more than
+    // the one chunk load the ring keeps in flight.  QS_JIT_L2PF: A/B knob.
+    static const int l2pf = getenv("QS_JIT_L2PF") ? atoi(getenv("QS_JIT_L2PF")) : 0;
+    const int PF = pipe ? l2pf : 0;
+    if (PF > 0) {
+      o << "__device__ __forceinline__ void l2pf(const double2* __restrict__ state, u64 chunk, u32 lane) {\n"
+        << "  const u64 cb = " << cbexpr << ";\n"
+        << "  for (int seg = (int)lane; seg < " << nseg << "; seg += 32) {\n"
+        << "    const u64 off = 0ull";
+      for (int i = 0; i < kChunkBits - l; i++)
+        o << " | ((u64)((seg >> " << i << ") & 1) << " << (int)h.cpos[l + i] << ")";
+      o << ";\n    asm volatile(\"cp.async.bulk.prefetch.L2.global [%0], %1;\" :: \"l\"(state + (cb | off)), \"r\"("
+        << (16 << l) << "u) : \"memory\");\n  }\n}\n";
+    }
     nthreads = kThreads * NG;
     const size_t npool = (h.total_bytes - h.off_pool) / sizeof(double);
     param_pool = npool > 0 && npool <= kMaxParamPool;
@@ -1086,6 +1102,9 @@ struct Gen {
         << "    if (" << chunk_of("k") << " < " << N << ") { issue_async(state, corder(" << chunk_of("k") << ")"
         << ", bufs + k * " << CH << ", mbar + k, tpd, sd); if (tid == 0) issued[k] = 1u; }\n";
     }
+    if (PF > 0)
+      o << "  for (u32 k = " << NB << "u + grp; k < " << NB + PF << "u; k += " << NG << "u)\n"
+        << "    if (tid < 32 && " << chunk_of("k") << " < " << N << ") l2pf(state, corder(" << chunk_of("k") << "), tid);\n";
     // level 1, constant shapes: once
     // level 1: one warp per shape, lanes over its terms, shuffle reduction
     auto level1 = [&](const char* map, size_t n, bool use_cphys) {
@@ -1139,15 +1158,18 @@ struct Gen {
     if (pipe) o << "    const u32 kb = k % " << NB << "u;\n    double2* const sch = bufs + kb * " << CH << ";\n";
     else if (xchg) o << "    double2* const sch = bufs + grp * " << CH << ";\n";
     const std::string nxt = chunk_of("k + " + std::to_string(NB));
+    const std::string pfc = chunk_of("k + " + std::to_string(NB + PF));
+    const std::string pf_issue =
+        PF > 0 ? "    if (tid < 32 && " + pfc + " < " + N + ") l2pf(state, corder(" + pfc + "), tid);\n" : "";
     const std::string count = "if (tid == 0) { __threadfence_block(); issued[kb] = k / " +
                               std::to_string(NB) + "u + 2u; }";
     const std::string refill =
         use_tma ? "    gbar(1u + grp);  // every thread is done reading the buffer\n"
                   "    if (tid < 32 && " + nxt + " < " + N +
-                  ") { fence_proxy_async(); issue(state, corder(" + nxt + "), sch, mbar + kb, tid, &tensmap); " + count + " }\n"
+                  ") { fence_proxy_async(); issue(state, corder(" + nxt + "), sch, mbar + kb, tid, &tensmap); " + count + " }\n" + pf_issue
                 : "    gbar(1u + grp);  // every thread is done reading the buffer\n"
                   "    if (" + nxt + " < " + N + ") { issue_async(state, corder(" + nxt + "), sch, mbar + kb, tpd, sd); " +
-                  count + " }\n";
+                  count + " }\n" + pf_issue;
     o << "    const u64 cb = " << cbexpr << ";\n";
     o << "    const u64 cphys = cb | rank_base;\n    (void)cphys;\n";
     // (cp.async row prefetch unless the pass's own chunk refill uses
@@ -1396,6 +1418,7 @@ struct Compiled {
 std::mutex g_mu;
 std::unordered_map<u64, Compiled> g_cache;  // key: hash ^ device
 std::unordered_map<void*, int> g_threads;   // function -> threads per CTA
+std::unordered_map<u64, u64> g_blob_src;    // descriptor bytes hash -> source hash
 double g_compile_ms = 0;
 uint64_t g_compiles = 0, g_disk_hits = 0;
 
@@ -1543,14 +1566,53 @@ int jit_prepare_all(const std::vector<const unsigned char*>& blobs, int device,
                     std::vector<JitPrepared>& out, bool compile_only) {
   const size_t n = blobs.size();
   out.assign(n, JitPrepared());
+  // Fast path: a descriptor seen before (same bytes: structure AND numbers,
+  // e.g. the same circuit again) whose kernel is loaded on this device needs
+  // no source generation at all.
+  std::vector<u64> bh(n);
+  std::vector<char> need(n, 1);
+  size_t n_need = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (size_t i = 0; i < n; i++) {
+      KPass hh;
+      memcpy(&hh, blobs[i], sizeof hh);
+      bh[i] = fnv1a(std::string(reinterpret_cast<const char*>(blobs[i]), hh.total_bytes));
+      auto it = g_blob_src.find(bh[i]);
+      if (!compile_only && it != g_blob_src.end()) {
+        auto c = g_cache.find(it->second ^ ((u64)(device + 1) * 0x9E3779B97F4A7C15ull));
+        if (c != g_cache.end()) {
+          JitPrepared& P = out[i];
+          P.ok = true;
+          P.fn = (void*)c->second.f;
+          P.per_sm = c->second.blocks_per_sm;
+          P.smem = c->second.smem;
+          P.threads = c->second.threads;
+          P.variant = c->second.variant;
+          need[i] = 0;
+          continue;
+        }
+      }
+      n_need++;
+    }
+  }
+  if (n_need == 0) return 0;
   std::vector<Source> srcs(n);
-  parallel_for(n, [&](size_t i) { srcs[i] = make_source(blobs[i]); });
+  std::vector<size_t> todo;
+  for (size_t i = 0; i < n; i++)
+    if (need[i]) todo.push_back(i);
+  parallel_for(todo.size(), [&](size_t t) { srcs[todo[t]] = make_source(blobs[todo[t]]); });
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (size_t i : todo)
+      if (srcs[i].ok) g_blob_src[bh[i]] = srcs[i].hash;
+  }
   // unique sources that are not loaded on this device yet
   std::map<u64, size_t> uniq;  // hash -> first pass index
   {
     std::lock_guard<std::mutex> lk(g_mu);
     for (size_t i = 0; i < n; i++) {
-      if (!srcs[i].ok) continue;
+      if (!need[i] || !srcs[i].ok) continue;
       const u64 key = srcs[i].hash ^ ((u64)(device + 1) * 0x9E3779B97F4A7C15ull);
       if (!compile_only && g_cache.count(key)) continue;
       uniq.emplace(srcs[i].hash, i);
@@ -1604,6 +1666,7 @@ int jit_prepare_all(const std::vector<const unsigned char*>& blobs, int device,
   if (compile_only) {
     for (size_t i = 0; i < n; i++) {
       JitPrepared& P = out[i];
+      if (!need[i]) continue;
       P.variant = srcs[i].variant;
       P.threads = srcs[i].threads;
       P.smem = srcs[i].smem;
@@ -1643,7 +1706,9 @@ int jit_prepare_all(const std::vector<const unsigned char*>& blobs, int device,
   }
   for (size_t i = 0; i < n; i++) {
     JitPrepared& P = out[i];
-    if (!srcs[i].ok) {
+    if (!need[i]) {
+      continue;
+    } else if (!srcs[i].ok) {
       P.err = srcs[i].err;
     } else if (failed.count(srcs[i].hash)) {
       P.err = failed[srcs[i].hash];
