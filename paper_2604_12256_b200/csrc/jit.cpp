@@ -307,6 +307,30 @@ struct Gen {
     }
     return "cks[" + std::to_string(k) + "]";
   }
+  // Dense-op matrix entries from a per-CTA shared-memory copy (csm[]) instead
+  // of constant-bank operands: QS_JIT_MSMEM=1 (A/B knob; measured worse).
+  std::map<int, int> m_slot;   // pool offset (doubles) -> csm index
+  bool mat_smem = false;
+  std::string mat_ref(int off) {
+    if (!mat_smem) return pv(off);
+    auto it = m_slot.find(off);
+    int k;
+    if (it == m_slot.end()) {
+      k = (int)m_slot.size();
+      m_slot[off] = k;
+    } else {
+      k = it->second;
+    }
+    return "csm[" + std::to_string(k) + "]";
+  }
+  int n_mat_doubles() const {  // upper bound of the register ops' matrix entries
+    int c = 0;
+    for (int i = 0; i < h.n_ops; i++) {
+      const int t = ops[i].type;
+      c += t == OP_D1 ? 8 : t == OP_D2 ? 32 : t == OP_D3 ? 128 : 0;
+    }
+    return c;
+  }
   int n_ck_entries() const {  // upper bound, before generation
     int c = 0;
     for (int i = 0; i < h.n_ops; i++)
@@ -450,12 +474,12 @@ struct Gen {
       kind[i] = (re == 0.0 && im == 0.0) ? 0 : (im == 0.0) ? 1 : (re == 0.0) ? 2 : 3;
       const std::string e = std::to_string(i);
       if (W <= 2) {
-        if (kind[i] == 1 || kind[i] == 3) o << "    const double mr" << e << " = " << pv(op.data + 2 * i) << ";\n";
-        if (kind[i] == 2 || kind[i] == 3) o << "    const double mi" << e << " = " << pv(op.data + 2 * i + 1) << ";\n";
+        if (kind[i] == 1 || kind[i] == 3) o << "    const double mr" << e << " = " << mat_ref(op.data + 2 * i) << ";\n";
+        if (kind[i] == 2 || kind[i] == 3) o << "    const double mi" << e << " = " << mat_ref(op.data + 2 * i + 1) << ";\n";
       }
     }
-    auto mr = [&](int i) { return (W <= 2) ? "mr" + std::to_string(i) : pv(op.data + 2 * i); };
-    auto mi = [&](int i) { return (W <= 2) ? "mi" + std::to_string(i) : pv(op.data + 2 * i + 1); };
+    auto mr = [&](int i) { return (W <= 2) ? "mr" + std::to_string(i) : mat_ref(op.data + 2 * i); };
+    auto mi = [&](int i) { return (W <= 2) ? "mi" + std::to_string(i) : mat_ref(op.data + 2 * i + 1); };
     for (int base = 0; base < kNReg; base++) {
       if (base & tm) continue;
       if ((base & (int)op.rcm) != (int)op.rcm) continue;
@@ -837,6 +861,11 @@ struct Gen {
     const int nlay = (int)L.size();
     const bool xchg = nlay > 1;  // any shared-memory exchange
     ck_smem = !xchg;
+    {
+      static const int msm = getenv("QS_JIT_MSMEM") ? atoi(getenv("QS_JIT_MSMEM")) : -1;  // A/B knob
+      mat_smem = msm > 0;  // default off: on the QAOA/rand-30 passes it spills MORE
+                           // (54 of 62 kernels, 8.9 KB vs 10 kernels, 0.6 KB)
+    }
     const int nsh = h.n_shapes;
     std::vector<int> vary, cons;
     for (int j = 0; j < nsh; j++) {
@@ -1003,7 +1032,13 @@ struct Gen {
     // group computes.  Write-only passes need a buffer per group only for
     // their layout exchanges.
     const int NG = groups_per_cta(pipe, nlay);
-    const int NB = pipe ? (NG == 1 ? 1 : NG + 1) : (xchg ? NG : 0);
+    int NB = pipe ? (NG == 1 ? 1 : NG + 1) : (xchg ? NG : 0);
+    {
+      // QS_JIT_NB: A/B knob for the ring depth of multi-layout load passes
+      // (more chunk loads in flight per SM)
+      static const int nb_env = getenv("QS_JIT_NB") ? atoi(getenv("QS_JIT_NB")) : 0;
+      if (pipe && xchg && nb_env > NB && (size_t)nb_env * CH * 16 <= 200 * 1024) NB = nb_env;
+    }
     // L2 prefetch distance (chunks of the CTA's sequence beyond the
     // shared-memory ring): cp.async.bulk.prefetch.L2 of chunk k + NB + PF
     // when chunk k's buffer is refilled, so DRAM latency overlaps more than
@@ -1063,7 +1098,7 @@ struct Gen {
     // of 228 KB, less the per-CTA reservation), minus the 4 KB sincos table
     // unless no sincos is left inside the loop (second generation pass)
     const long smem_cap = ((NG == 1 && NB <= 1) ? 113 * 1024 : 227 * 1024) - (table_free ? 0 : 4096) -
-                          (ck_smem ? 16l * n_ck_entries() : 0l);
+                          (ck_smem ? 16l * n_ck_entries() : 0l) - (mat_smem ? 8l * n_mat_doubles() : 0l);
     max_hoist = (int)std::max<long>(0, (smem_cap - (long)hz_off) / (kThreads * 16));
     if (max_hoist > 24) max_hoist = 24;
     if (const char* e = getenv("QS_JIT_MAXHOIST")) max_hoist = std::min(max_hoist, atoi(e));  // experiments
@@ -1221,7 +1256,52 @@ struct Gen {
     for (int r = 0; r < kNReg; r++) nm[r] = r;
     pend_c.clear();
     pend_scale = (h.scale != 1.0);
-    if (h.src_mode == 1) {
+    static const bool xsm_off = getenv("QS_JIT_NOXSM") != nullptr;  // A/B knob
+    if (h.src_mode == 1 && xchg && !xsm_off) {
+      // Multi-layout write-only pass: the tensor product is expanded into the
+      // chunk buffer in LINEAR chunk order (thread t makes chunk elements
+      // t + 256 i), so consecutive lanes gather consecutive sub-state entries
+      // (coalesced, L1-friendly), then layout 0 is read from the buffer like
+      // an exchange.  Groups with no chunk position are per-chunk constants.
+      u64 cmask = 0;
+      for (int c = 0; c < kChunkBits; c++) cmask |= 1ull << h.cpos[c];
+      std::vector<int> varying;
+      std::string tpd = "(0ull";
+      for (int i = 0; i < kLogT; i++)
+        tpd += " | ((u64)((tid >> " + std::to_string(i) + ") & 1u) << " + std::to_string((int)h.cpos[i]) + ")";
+      tpd += ")";
+      for (int g = 0; g < h.expand.n; g++) {
+        o << "    const double2* __restrict__ sv" << g << " = reinterpret_cast<const double2*>(*reinterpret_cast<const u64*>(blob + "
+          << (size_t)((const unsigned char*)&h.expand.ptr[g] - (const unsigned char*)&h) << "));\n";
+        const u64 gmask = ((1ull << h.expand.len[g]) - 1) << h.expand.lo[g];
+        if (cmask & gmask) {
+          varying.push_back(g);
+        } else {
+          o << "    const double2 pf" << g << " = __ldg(sv" << g << " + ((cphys >> " << h.expand.lo[g] << ") & "
+            << u((1ull << h.expand.len[g]) - 1) << "));\n";
+          pend_c.push_back("pf" + std::to_string(g));
+        }
+      }
+      // (the group may still be reading the previous chunk's last layout)
+      o << "    gbar(1u + grp);\n    { const u64 xb = cphys | " << tpd << ";\n";
+      for (int i = 0; i < kNReg; i++) {
+        u64 off = 0;
+        for (int k = 0; k < kRegBits; k++)
+          if (i >> k & 1) off |= 1ull << h.cpos[kLogT + k];
+        o << "      { const u64 ph = xb | " << u(off) << "; double2 v = ";
+        if (varying.empty()) o << "make_double2(1.0, 0.0)";
+        for (size_t q = 0; q < varying.size(); q++) {
+          const int g = varying[q];
+          const std::string ld = "__ldg(sv" + std::to_string(g) + " + ((ph >> " + std::to_string(h.expand.lo[g]) +
+                                 ") & " + u((1ull << h.expand.len[g]) - 1) + "))";
+          if (q == 0) o << ld;
+          else o << "; v = cmul(v, " << ld << ")";
+        }
+        o << "; sch[swz((int)tid ^ " << (i << kLogT) << ")] = v; }\n";
+      }
+      o << "    }\n    gbar(1u + grp);\n";
+      for (int r = 0; r < kNReg; r++) o << "    " << A(r) << " = sch[st0 ^ " << reg_slot(0, r) << "];\n";
+    } else if (h.src_mode == 1) {
       // groups whose sub-state index ignores the register bits contribute a
       // per-thread constant factor (loaded once, folded later)
       u64 regpos = 0;
@@ -1343,6 +1423,23 @@ struct Gen {
     o << "}\n";
     std::string s = o.str();
     if (n_hoist) s.insert(loop_pos, "  if (grp == 0) {\n" + pre.str() + "  }\n  __syncthreads();\n");
+    if (!m_slot.empty()) {
+      std::string t = "  __shared__ double csm[" + std::to_string(m_slot.size()) + "];\n  {\n";
+      t += "    const unsigned short csoff[" + std::to_string(m_slot.size()) + "] = {";
+      bool first = true;
+      for (auto& kv : m_slot) {  // m_slot is ordered by offset; indices by first use
+        (void)kv;
+      }
+      std::vector<int> offs(m_slot.size());
+      for (auto& kv : m_slot) offs[kv.second] = kv.first;
+      for (int v : offs) {
+        t += (first ? "" : ",") + std::to_string(v);
+        first = false;
+      }
+      t += "};\n    for (int i = (int)threadIdx.x; i < " + std::to_string(m_slot.size()) + "; i += " +
+           std::to_string(nthreads) + ") csm[i] = __ldg(pool + csoff[i]);\n  }\n";
+      s.insert(ctab_pos, t);
+    }
     if (!ck_slot.empty()) {
       std::string t = "  __shared__ double2 cks[" + std::to_string(ck_slot.size()) + "];\n  {\n";
       for (auto& kv : ck_slot)
