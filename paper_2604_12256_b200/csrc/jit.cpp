@@ -361,6 +361,8 @@ struct Gen {
   static int groups_per_cta(bool pipe, int nlay) {
     const char* e = getenv("QS_JIT_GROUPS");
     if (e && (atoi(e) == 1 || atoi(e) == 2)) return atoi(e);
+    const char* w = getenv("QS_JIT_WO_GROUPS");  // A/B knob: write-only passes
+    if (!pipe && w && (atoi(w) == 1 || atoi(w) == 2)) return atoi(w);
     return (pipe && nlay > 1) ? 2 : 1;
   }
   Gen(const KPass& hh, const unsigned char* blob)
