@@ -23,6 +23,8 @@
 #include <unistd.h>
 
 #include <chrono>
+#include <functional>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -124,6 +126,22 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 // the mbarrier sees one arrival once all of this thread's prior cp.async land
 __device__ __forceinline__ void cp_async_mbar_arrive(u64* b) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(sa(b)) : "memory");
+}
+// exact unit (1, i, -1, -i) -> quarter index 0..3 (integer bit tests)
+__device__ __forceinline__ u32 qof(double2 e) {
+  const u64 bx = (u64)__double_as_longlong(e.x), by = (u64)__double_as_longlong(e.y);
+  const u32 sw = (bx << 1) == 0ull ? 1u : 0u;
+  const u32 ng = (u32)((sw ? by : bx) >> 63);
+  return sw | (ng << 1);
+}
+// a * i^q by sign/swap of the bit patterns (no FP64 instruction)
+__device__ __forceinline__ double2 rotq(double2 a, u32 q) {
+  const u64 ax = (u64)__double_as_longlong(a.x), ay = (u64)__double_as_longlong(a.y);
+  const bool s = (q & 1u) != 0u;
+  const u64 sg = (u64)((q >> 1) & 1u) << 63;
+  const u64 nx = (s ? (ay ^ 0x8000000000000000ull) : ax) ^ sg;
+  const u64 ny = (s ? ax : ay) ^ sg;
+  return make_double2(__longlong_as_double((long long)nx), __longlong_as_double((long long)ny));
 }
 // barrier of one 256-thread chunk group (named barrier 1 + group)
 __device__ __forceinline__ void gbar(u32 id) { asm volatile("bar.sync %0, 256;" :: "r"(id) : "memory"); }
@@ -280,6 +298,8 @@ struct Gen {
   // folded into the next full-width diagonal's E0, else applied at the store
   std::vector<std::string> pend_c;
   bool pend_scale = false;
+  int sc_kind = 0, sc_sx = 1, sc_sy = 1;  // unit part of the pass scale (see build)
+  double sc_mag = 1.0;                     // its real magnitude (folded like the H scale)
   // pass constants (matrices, CK tables) as a by-value kernel parameter:
   // FP64 instructions then read them as constant-bank operands
   bool param_pool = false;
@@ -361,9 +381,12 @@ struct Gen {
   static int groups_per_cta(bool pipe, int nlay) {
     const char* e = getenv("QS_JIT_GROUPS");
     if (e && (atoi(e) == 1 || atoi(e) == 2)) return atoi(e);
-    const char* w = getenv("QS_JIT_WO_GROUPS");  // A/B knob: write-only passes
-    if (!pipe && w && (atoi(w) == 1 || atoi(w) == 2)) return atoi(w);
-    return (pipe && nlay > 1) ? 2 : 1;
+    // write-only passes: two groups per CTA too (QFT-30's K2 3.73 -> 3.37 ms:
+    // the groups share the CTA's hoisted per-thread values); QS_JIT_WO_GROUPS
+    // is the A/B knob
+    const char* w = getenv("QS_JIT_WO_GROUPS");
+    if (!pipe) return (w && atoi(w) == 1) ? 1 : 2;
+    return nlay > 1 ? 2 : 1;
   }
   Gen(const KPass& hh, const unsigned char* blob)
       : h(hh),
@@ -470,10 +493,14 @@ struct Gen {
     // code -- e.g. RX, RY, SX need 4 FP64 per output instead of 8; values stay
     // run-time data.
     const double* mv = pool + op.data;
-    std::vector<int> kind(D * D);  // 0 zero, 1 real, 2 imag, 3 complex
+    // 0 zero, 1 real, 2 imag, 3 complex; exact units (unit-scaled ops,
+    // encode_pass): 4 +1, 5 -1, 6 +i, 7 -i -- additions only
+    std::vector<int> kind(D * D);
     for (int i = 0; i < D * D; i++) {
       const double re = mv[2 * i], im = mv[2 * i + 1];
-      kind[i] = (re == 0.0 && im == 0.0) ? 0 : (im == 0.0) ? 1 : (re == 0.0) ? 2 : 3;
+      kind[i] = (re == 0.0 && im == 0.0) ? 0 : (im == 0.0 && re == 1.0) ? 4 : (im == 0.0 && re == -1.0) ? 5
+              : (re == 0.0 && im == 1.0) ? 6 : (re == 0.0 && im == -1.0) ? 7
+              : (im == 0.0) ? 1 : (re == 0.0) ? 2 : 3;
       const std::string e = std::to_string(i);
       if (W <= 2) {
         if (kind[i] == 1 || kind[i] == 3) o << "    const double mr" << e << " = " << mat_ref(op.data + 2 * i) << ";\n";
@@ -518,6 +545,22 @@ struct Gen {
               add(im, mr(i) + " * " + v + ".y", false);
               add(im, mi(i) + " * " + v + ".x", false);
               break;
+            case 4:  // +1
+              add(re, v + ".x", false);
+              add(im, v + ".y", false);
+              break;
+            case 5:  // -1
+              add(re, v + ".x", true);
+              add(im, v + ".y", true);
+              break;
+            case 6:  // +i: i (x + iy) = -y + ix
+              add(re, v + ".y", true);
+              add(im, v + ".x", false);
+              break;
+            case 7:  // -i
+              add(re, v + ".y", false);
+              add(im, v + ".x", true);
+              break;
             default:
               break;
           }
@@ -540,7 +583,7 @@ struct Gen {
     std::string f;
     if (norm) f = "0x1.6a09e667f3bcdp-1";
     else if (pend_scale && op.rcm == 0 && op.ncm == 0) {
-      f = hex(h.scale);
+      f = hex(sc_mag);
       pend_scale = false;
     }
     for (int r = 0; r < kNReg; r++) {
@@ -603,6 +646,27 @@ struct Gen {
     return s;
   }
 
+  // quarter index of an exact unit (1, i, -1, -i -> 0..3); -1 otherwise
+  static int unit_q(double re, double im) {
+    if (re == 1.0 && im == 0.0) return 0;
+    if (re == 0.0 && im == 1.0) return 1;
+    if (re == -1.0 && im == 0.0) return 2;
+    if (re == 0.0 && im == -1.0) return 3;
+    return -1;
+  }
+  bool quarter_group(const KGroup& G) const {
+    static const bool off = getenv("QS_JIT_NOQUARTER") != nullptr;  // A/B knob
+    if (off) return false;
+    for (int j = G.rbeg[0]; j < G.rbeg[kNReg]; j++)
+      for (int q = shapes[j].term_begin; q < shapes[j].term_end; q++)
+        if (terms[q].coeff & ((1ull << 62) - 1)) return false;
+    if (G.ck_off >= 0)
+      for (int r = 0; r < kNReg; r++)
+        if (unit_q(pool[G.ck_off + 2 * r], pool[G.ck_off + 2 * r + 1]) < 0) return false;
+    return true;
+  }
+  bool uses_rotq = false;
+
   void diag_fast(const KOp& op) {
     const KGroup& G = groups[op.data];
     const int L = op.sel;
@@ -652,12 +716,62 @@ struct Gen {
       n_table++;
       return "cis_tab(" + shape_sum(G, R) + ", ctab)";
     };
+    // Quarter-turn group (every coefficient a multiple of 1/4 turn, e.g. CZ,
+    // S, CP(pi/2) chains): every factor is exactly one of 1, i, -1, -i, so the
+    // phases are applied with integer sign/swap operations on the amplitude
+    // bits (rotq) instead of FP64 complex products.
+    if (quarter_group(G)) {
+      // the quarter index of a factor: straight from its angle (top 2 bits)
+      // when it is summed here, else from the exact unit value
+      std::function<std::string(const std::string&)> qv = [&](const std::string& e) -> std::string {
+        const std::string tab = "cis_tab(", suf = ", ctab)";
+        if (e.compare(0, tab.size(), tab) == 0 && e.size() > tab.size() + suf.size() &&
+            e.compare(e.size() - suf.size(), suf.size(), suf) == 0) {
+          n_table--;  // no sincos needed
+          return "((u32)((" + e.substr(tab.size(), e.size() - tab.size() - suf.size()) + ") >> 62))";
+        }
+        const std::string cm = "cmul(";
+        if (e.compare(0, cm.size(), cm) == 0) {  // cmul(thread part, table column): two exact units
+          const size_t c = e.rfind(", ");
+          return "(" + qv(e.substr(cm.size(), c - cm.size())) + " + " + qv(e.substr(c + 2, e.size() - c - 3)) + ")";
+        }
+        return "qof(" + e + ")";
+      };
+      o << "    u32 Q = 0u;\n";
+      if (hc) o << "    Q = " << qv(evar(0)) << ";\n";
+      std::vector<int> lbq;
+      for (int k = 0; k < kRegBits; k++)
+        if (L >> k & 1) {
+          lbq.push_back(k);
+          o << "    const u32 Q" << k + 1 << " = " << qv(evar(1 << k)) << ";\n";
+        }
+      uses_rotq = true;
+      const int m = (int)lbq.size();
+      for (int i = 0; i < (1 << m); i++) {
+        const int g = i ^ (i >> 1);
+        if (i > 0) {
+          const int b = __builtin_ctz(g ^ ((i - 1) ^ ((i - 1) >> 1)));
+          o << "    Q = (Q " << ((g >> b & 1) ? "+" : "-") << " Q" << lbq[b] + 1 << ") & 3u;\n";
+        }
+        int sub = 0;
+        for (int t = 0; t < m; t++)
+          if (g >> t & 1) sub |= 1 << lbq[t];
+        for (int r = 0; r < kNReg; r++) {
+          if (!(op.rcm >> r & 1) || (r & L) != sub) continue;
+          int cq = 0;
+          if (G.ck_off >= 0) cq = unit_q(pool[G.ck_off + 2 * r], pool[G.ck_off + 2 * r + 1]);
+          o << "    " << A(r) << " = rotq(" << A(r) << ", Q + " << cq << "u);\n";
+        }
+      }
+      o << "  }\n";
+      return;
+    }
     if (hc) {
       o << "    double2 E0 = " << evar(0) << ";\n";
       if (op.rcm == 0xFFFFu) {  // multiplies every register: absorb pending factors
         for (const std::string& f : pend_c) o << "    E0 = cmul(E0, " << f << ");\n";
         if (pend_scale)
-          o << "    E0 = make_double2(E0.x * " << hex(h.scale) << ", E0.y * " << hex(h.scale) << ");\n";
+          o << "    E0 = make_double2(E0.x * " << hex(sc_mag) << ", E0.y * " << hex(sc_mag) << ");\n";
         pend_c.clear();
         pend_scale = false;
       }
@@ -1200,13 +1314,22 @@ struct Gen {
         PF > 0 ? "    if (tid < 32 && " + pfc + " < " + N + ") l2pf(state, corder(" + pfc + "), tid);\n" : "";
     const std::string count = "if (tid == 0) { __threadfence_block(); issued[kb] = k / " +
                               std::to_string(NB) + "u + 2u; }";
-    const std::string refill =
-        use_tma ? "    gbar(1u + grp);  // every thread is done reading the buffer\n"
+    // QS_JIT_CHECK (debug builds of the kernels; compute-sanitizer is not
+    // available on the GPU pool): the consumed buffer is overwritten with NaN
+    // before its refill is issued, so a read that races the refill (or a
+    // stale-phase wait) poisons the result instead of silently reusing data;
+    // and the ring's phase bookkeeping is asserted (trap on violation).
+    static const bool check = getenv("QS_JIT_CHECK") != nullptr;
+    const std::string poison =
+        check ? "    gbar(1u + grp);\n    for (int i = 0; i < 16; i++) sch[(int)tid + 256 * i] = make_double2(__longlong_as_double(0x7ff8dead7ff8deadll), __longlong_as_double(0x7ff8dead7ff8deadll));\n"
+              : "";
+    const std::string refill = poison +
+        (use_tma ? "    gbar(1u + grp);  // every thread is done reading the buffer\n"
                   "    if (tid < 32 && " + nxt + " < " + N +
                   ") { fence_proxy_async(); issue(state, corder(" + nxt + "), sch, mbar + kb, tid, &tensmap); " + count + " }\n" + pf_issue
                 : "    gbar(1u + grp);  // every thread is done reading the buffer\n"
                   "    if (" + nxt + " < " + N + ") { issue_async(state, corder(" + nxt + "), sch, mbar + kb, tpd, sd); " +
-                  count + " }\n" + pf_issue;
+                  count + " }\n" + pf_issue);
     o << "    const u64 cb = " << cbexpr << ";\n";
     o << "    const u64 cphys = cb | rank_base;\n    (void)cphys;\n";
     // (cp.async row prefetch unless the pass's own chunk refill uses
@@ -1257,7 +1380,18 @@ struct Gen {
     // loads (phase 0)
     for (int r = 0; r < kNReg; r++) nm[r] = r;
     pend_c.clear();
-    pend_scale = (h.scale != 1.0);
+    // pass scale S = (scale, scale_im) = m * u: the real m is folded into an
+    // unnormalised H / a full-width diagonal / the store as before; the unit
+    // u is applied at the end: +-1 (sign of m), +-i (swap + sign), an eighth
+    // turn (+-1 +- i)/|.| (two additions), else a constant complex product
+    {
+      const double sr = h.scale, si = h.scale_im;
+      if (si == 0.0) { sc_kind = 0; sc_mag = sr; }
+      else if (sr == 0.0) { sc_kind = 1; sc_mag = si; }                          // S = i * si
+      else if (std::fabs(sr) == std::fabs(si)) { sc_kind = 2; sc_mag = std::fabs(sr); sc_sx = sr > 0 ? 1 : -1; sc_sy = si > 0 ? 1 : -1; }
+      else { sc_kind = 3; sc_mag = 1.0; }
+    }
+    pend_scale = (sc_mag != 1.0);
     static const bool xsm_off = getenv("QS_JIT_NOXSM") != nullptr;  // A/B knob
     if (h.src_mode == 1 && xchg && !xsm_off) {
       // Multi-layout write-only pass: the tensor product is expanded into the
@@ -1355,6 +1489,7 @@ struct Gen {
       // j - 1 was consumed, so first wait until it has been issued.
       if (NG > 1) o << "    while (issued[kb] < k / " << NB << "u + 1u) {}\n";
       o << "    mbar_wait(mbar + kb, (k / " << NB << "u) & 1u);\n";
+      if (check && NG > 1) o << "    if (issued[kb] != k / " << NB << "u + 1u) __trap();\n";
       if (use_tma) {
         for (int r = 0; r < kNReg; r++) {
           int rc = 0;
@@ -1386,13 +1521,29 @@ struct Gen {
     if (!pend_c.empty()) {
       o << "    { double2 F = " << pend_c[0] << ";\n";
       for (size_t i = 1; i < pend_c.size(); i++) o << "      F = cmul(F, " << pend_c[i] << ");\n";
-      if (pend_scale) o << "      F = make_double2(F.x * " << hex(h.scale) << ", F.y * " << hex(h.scale) << ");\n";
+      if (pend_scale) o << "      F = make_double2(F.x * " << hex(sc_mag) << ", F.y * " << hex(sc_mag) << ");\n";
       for (int r = 0; r < kNReg; r++) o << "      " << A(r) << " = cmul(" << A(r) << ", F);\n";
       o << "    }\n";
     } else if (pend_scale) {
       for (int r = 0; r < kNReg; r++)
-        o << "    " << A(r) << " = make_double2(" << A(r) << ".x * " << hex(h.scale) << ", " << A(r)
-          << ".y * " << hex(h.scale) << ");\n";
+        o << "    " << A(r) << " = make_double2(" << A(r) << ".x * " << hex(sc_mag) << ", " << A(r)
+          << ".y * " << hex(sc_mag) << ");\n";
+    }
+    if (sc_kind == 1) {         // * i
+      for (int r = 0; r < kNReg; r++)
+        o << "    " << A(r) << " = make_double2(-" << A(r) << ".y, " << A(r) << ".x);\n";
+    } else if (sc_kind == 2) {  // * (sx + i sy), magnitude folded
+      const char* px = sc_sx > 0 ? "" : "-";
+      const char* py = sc_sy > 0 ? "" : "-";
+      for (int r = 0; r < kNReg; r++)
+        o << "    " << A(r) << " = make_double2(" << px << A(r) << ".x - " << py << "(" << A(r) << ".y), "
+          << py << A(r) << ".x + " << px << "(" << A(r) << ".y));\n";
+    } else if (sc_kind == 3) {  // general complex scale (read from the descriptor)
+      o << "    { const double2 S = make_double2(*reinterpret_cast<const double*>(blob + "
+        << (size_t)((const unsigned char*)&h.scale - (const unsigned char*)&h) << "), *reinterpret_cast<const double*>(blob + "
+        << (size_t)((const unsigned char*)&h.scale_im - (const unsigned char*)&h) << "));\n";
+      for (int r = 0; r < kNReg; r++) o << "      " << A(r) << " = cmul(" << A(r) << ", S);\n";
+      o << "    }\n";
     }
     if (h.x_mask) {
       // exported piece s = the output index's top x_j local bits; they may

@@ -553,7 +553,11 @@ qs_kpass(const unsigned char* __restrict__ blob, double2* __restrict__ state) {
     }
     Layout O;
     make_layout(P, nph - 1, tid, true, O);
-    if (P.scale != 1.0) {
+    if (P.scale_im != 0.0) {
+      const double2 sc = make_double2(P.scale, P.scale_im);
+#pragma unroll
+      for (int r = 0; r < kNReg; r++) a[r] = cmul(a[r], sc);
+    } else if (P.scale != 1.0) {
       const double sc = P.scale;
 #pragma unroll
       for (int r = 0; r < kNReg; r++) a[r] = make_double2(a[r].x * sc, a[r].y * sc);

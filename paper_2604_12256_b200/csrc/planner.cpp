@@ -179,7 +179,51 @@ static double mat_cost(const std::vector<cd>& m) {
   for (const cd& z : m) c += (z == cd(0, 0)) ? 0.0 : (z.imag() == 0.0 || z.real() == 0.0) ? 2.0 : 4.0;
   return c / (double)D;
 }
+
+// A "unit-scaled" matrix: every nonzero entry is exactly +-lam or +-i lam
+// for one complex lam (the first nonzero entry), e.g. SX = ((1+i)/2) [[1,-i],
+// [-i,1]], SY = ((1+i)/2) [[1,-1],[1,1]], CZ-free Clifford products.  For an
+// UNCONTROLLED op lam commutes with the whole pass (a global scalar of the
+// shard), so the kernels apply the +-1/+-i matrix with additions only and
+// fold lam into the pass scale (encode_pass).  unit_out (optional) receives
+// the +-1/+-i/0 matrix (exact: built from the comparison, not a division).
+static bool unit_scaled(const std::vector<cd>& m, cd* lam_out, std::vector<cd>* unit_out) {
+  cd lam(0, 0);
+  for (const cd& z : m)
+    if (z != cd(0, 0)) {
+      lam = z;
+      break;
+    }
+  if (lam == cd(0, 0)) return false;
+  const cd ilam(-lam.imag(), lam.real());  // i * lam, exact
+  if (unit_out) unit_out->assign(m.size(), cd(0, 0));
+  for (size_t k = 0; k < m.size(); k++) {
+    const cd z = m[k];
+    cd u;
+    if (z == cd(0, 0)) u = cd(0, 0);
+    else if (z == lam) u = cd(1, 0);
+    else if (z == -lam) u = cd(-1, 0);
+    else if (z == ilam) u = cd(0, 1);
+    else if (z == -ilam) u = cd(0, -1);
+    else return false;
+    if (unit_out) (*unit_out)[k] = u;
+  }
+  if (lam_out) *lam_out = lam;
+  return true;
+}
+
+// FP64 instructions per output amplitude of an UNCONTROLLED op: a
+// unit-scaled matrix needs only complex additions (nnz - 1 per row).
+static double mat_cost_unc(const std::vector<cd>& m) {
+  if (!unit_scaled(m, nullptr, nullptr)) return mat_cost(m);
+  size_t D = 1;
+  while (D * D < m.size()) D++;
+  size_t nnz = 0;
+  for (const cd& z : m) nnz += z != cd(0, 0);
+  return 2.0 * ((double)nnz / (double)D - 1.0);
+}
 static double op_cost(const std::vector<cd>& m, bool is_h) { return is_h ? 2.0 : mat_cost(m); }
+static double op_cost_unc(const std::vector<cd>& m, bool is_h) { return is_h ? 2.0 : mat_cost_unc(m); }
 
 // Emit the pending source as a standalone step (before a swap / small pass).
 static void flush_source(Sched& S) {
@@ -259,13 +303,13 @@ static void fuse_ops(std::vector<POp>& ops, int fuse_cap) {
       size_t j = i + 1;
       u64 um = 0;
       for (int p : ops[i].tpos) um |= 1ull << p;
-      double parts = op_cost(ops[i].mat, ops[i].is_h);
+      double parts = op_cost_unc(ops[i].mat, ops[i].is_h);
       while (j < ops.size() && fusable(ops[j])) {
         u64 nm = um;
         for (int p : ops[j].tpos) nm |= 1ull << p;
         if (popc(nm) > cap) break;
         um = nm;
-        parts += op_cost(ops[j].mat, ops[j].is_h);
+        parts += op_cost_unc(ops[j].mat, ops[j].is_h);
         j++;
       }
       if (j - i >= 3) {
@@ -276,7 +320,7 @@ static void fuse_ops(std::vector<POp>& ops, int fuse_cap) {
           f.tpos = uni;
           f.n_src += ops[q].n_src;
         }
-        if (mat_cost(f.mat) * (f.tpos.size() >= (size_t)kRegBits ? 2.0 : 1.0) <= parts) {
+        if (mat_cost_unc(f.mat) * (f.tpos.size() >= (size_t)kRegBits ? 2.0 : 1.0) <= parts) {
           f.is_h = f.is_x = false;
           out.push_back(std::move(f));
           i = j;
@@ -291,11 +335,11 @@ static void fuse_ops(std::vector<POp>& ops, int fuse_cap) {
       for (int p : prev.tpos) um |= 1ull << p;
       for (int p : op.tpos) um |= 1ull << p;
       const int ku = popc(um);
-      const double parts = op_cost(prev.mat, prev.is_h) + op_cost(op.mat, op.is_h);
+      const double parts = op_cost_unc(prev.mat, prev.is_h) + op_cost_unc(op.mat, op.is_h);
       if (ku <= pcap && dense_cost(ku) / 2 <= parts) {
         std::vector<int> uni;
         std::vector<cd> F = fuse_pair(prev, op, uni);
-        if (mat_cost(F) <= parts) {
+        if (mat_cost_unc(F) <= parts) {
           prev.mat = F;
           prev.tpos = uni;
           prev.is_h = prev.is_x = false;
@@ -651,7 +695,7 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
         const bool wide = (int)g.targets.size() >= kRegBits;  // 4-6 targets: shared-memory op
         u64 nn = need | tp;
         if (popc(nn) > kChunkBits) { defer(); continue; }
-        const double c = op_cost(g.mat, g.is_h) + 0.5;
+        const double c = (g.controls.empty() ? op_cost_unc(g.mat, g.is_h) : op_cost(g.mat, g.is_h)) + 0.5;
         if (cost + c > budget && dense_taken > 0) { stop = true; defer(); continue; }
         // register layouts (assign_phases' greedy, on positions): a new
         // layout costs a shared-memory exchange; keep <= kMaxPhases/2
@@ -1016,6 +1060,8 @@ int encode_pass(const PassPlan& p, int rank, std::vector<unsigned char>& out, st
     }
   }
   h.scale = 1.0;
+  h.scale_im = 0.0;
+  cd lam_total(1.0, 0.0);  // scalars factored out of unit-scaled ops
   if (p.x_j < 0 || p.x_j > kMaxXBits) {
     err = "internal: fused swap exports more than 3 qubits";
     return QS_EINVAL;
@@ -1201,6 +1247,15 @@ int encode_pass(const PassPlan& p, int rank, std::vector<unsigned char>& out, st
             }
             pm[(size_t)r2 * D + c2] = op.mat[(size_t)r * D + c];
           }
+        // uncontrolled unit-scaled op: +-1/+-i matrix, scalar into the pass scale
+        {
+          cd lam;
+          std::vector<cd> unit;
+          if (op.cmask == 0 && !op.is_h && !op.is_x && unit_scaled(pm, &lam, &unit)) {
+            pm.swap(unit);
+            lam_total *= lam;
+          }
+        }
         if (t == 1) {
           k.sel = (uint8_t)rbits[0];
           if (op.is_h && rcm == 0 && ncm == 0) {
@@ -1286,8 +1341,13 @@ int encode_pass(const PassPlan& p, int rank, std::vector<unsigned char>& out, st
                 nz = true;
               }
             if (nz) {
-              const long double th = (long double)ang / 18446744073709551616.0L * 6.283185307179586476925286766559L;
-              ck[r] = cd((double)cosl(th), (double)sinl(th));
+              if ((ang & ((1ull << 62) - 1)) == 0) {  // quarter turns: exact units
+                static const cd unit[4] = {cd(1, 0), cd(0, 1), cd(-1, 0), cd(0, -1)};
+                ck[r] = unit[ang >> 62];
+              } else {
+                const long double th = (long double)ang / 18446744073709551616.0L * 6.283185307179586476925286766559L;
+                ck[r] = cd((double)cosl(th), (double)sinl(th));
+              }
             }
             if (hc || (r & lin) || nz) touch |= 1u << r;
           }
@@ -1356,7 +1416,9 @@ int encode_pass(const PassPlan& p, int rank, std::vector<unsigned char>& out, st
     h.n_shapes = (int)kshapes.size();
     h.n_groups = (int)kgroups.size();
     // OP_HU leaves a factor sqrt2 per gate: restore 2^{-n_hu/2} at the store
-    h.scale = std::ldexp(1.0, -(n_hu / 2)) * ((n_hu & 1) ? 0.70710678118654752440 : 1.0);
+    const double hs = std::ldexp(1.0, -(n_hu / 2)) * ((n_hu & 1) ? 0.70710678118654752440 : 1.0);
+    h.scale = hs * lam_total.real();
+    h.scale_im = hs * lam_total.imag();
     if (h.n_shapes > kMaxShapes) {
       err = "internal: too many diagonal shapes in one pass";
       return QS_EINVAL;

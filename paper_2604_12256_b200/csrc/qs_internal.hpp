@@ -130,7 +130,9 @@ struct KPass {
   u64 rank_base;       // rank << nl
   u64 local_mask;      // (1 << nl) - 1
   u64 basis;           // src_mode 2: physical index of the 1.0 amplitude
-  double scale;        // multiplies every amplitude at the store (OP_HU)
+  double scale;        // (scale, scale_im) multiplies every amplitude: the
+  double scale_im;     // 2^{-1/2} of each OP_HU and the scalars factored out
+                       // of unit-scaled dense ops (encode_pass)
   int32_t x_shift, x_mask;  // fused swap export: x_mask = 2^j - 1 (0: none)
   int8_t x_pos[8];          // piece s = sum_i bit x_pos[i] of the local index << i
   int8_t cpos[16];     // physical position of chunk bit c (loads, ops)
