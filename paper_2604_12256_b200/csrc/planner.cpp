@@ -631,7 +631,7 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
     // the following read+write passes; other passes are capacity-limited.
     static const double wo_budget = [] {
       const char* e = getenv("QS_WO_BUDGET");  // experiment knob
-      return (e && *e) ? atof(e) : 48.0;
+      return (e && *e) ? atof(e) : 40.0;
     }();
     const double budget = (buf == 0 && S.src_mode && !small) ? wo_budget : 400.0;
     double cost = 0;

@@ -100,6 +100,22 @@ def main():
         print(json.dumps({"case": "rx_layers24", "world": world, "max_abs_diff": err, "swaps": st["n_swaps"], "fused_swaps": st["n_fused_swaps"],
                           "bytes_nvlink": st["bytes_nvlink"], "t_swap_ms": st["t_swap_ms"], "ok": ok}),
               flush=True)
+    # steady state at scale: QAOA and supremacy-style circuits on 26 qubits
+    # (>= 22 local qubits: specialised kernels, many chunks per CTA, fused
+    # swaps over NVLink peer stores), default configuration, vs the oracle
+    for name, n, gates in (("qaoa26", 26, W.qaoa_maxcut(26, 3, 26)),
+                           ("supremacy26", 26, W.supremacy_n(26, 8, 26))):
+        sim = qs.Simulator(n, rank=rank, world_size=world, device=local, nccl_id=new_id())
+        sim.apply(gates)
+        psi = sim.state()
+        st = sim.stats()
+        sim.close()
+        if rank == 0:
+            err = float(np.max(np.abs(psi - oracle.apply_circuit(n, gates))))
+            ok = err < 1e-12 and (world == 1 or st["n_swaps"] >= 1)
+            bad += not ok
+            print(json.dumps({"case": name, "world": world, "max_abs_diff": err, "swaps": st["n_swaps"],
+                              "fused_swaps": st["n_fused_swaps"], "passes": st["n_passes"], "ok": ok}), flush=True)
     dist.barrier()
     if rank == 0 and torch.cuda.device_count() >= world:
         # single-process multi-device mode (ncclCommInitAll)
