@@ -165,6 +165,7 @@ struct Sched {
                                     // 1 expand (booster), 2 basis
   std::vector<int> exp_bufs, exp_lo, exp_len;
   uint64_t basis_phys = 0;
+  double wo_budget = 40.0;          // FP64/amp budget of the write-only first pass (c15)
 };
 
 static double dense_cost(int k) { return 4.0 * (1 << k); }  // FP64 FMA per amp
@@ -629,11 +630,7 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
     // given about the FP64 work the HBM time of a write-only pass covers
     // (~48/amp at 6.5 TB/s and ~18 TFLOP/s FP64), so ALU-heavy work moves to
     // the following read+write passes; other passes are capacity-limited.
-    static const double wo_budget = [] {
-      const char* e = getenv("QS_WO_BUDGET");  // experiment knob
-      return (e && *e) ? atof(e) : 40.0;
-    }();
-    const double budget = (buf == 0 && S.src_mode && !small) ? wo_budget : 400.0;
+    const double budget = (buf == 0 && S.src_mode && !small) ? S.wo_budget : 400.0;
     double cost = 0;
     // Encoder limit (kMaxShapes diagonal shapes per pass).  A diagonal op's
     // shapes are at most its distinct physical masks, and neither the
@@ -983,8 +980,29 @@ static int booster(Sched& S, int n, std::vector<IrGate>& gates, std::string& err
 }
 
 // ------------------------------------------------------------ make_plan
+static int make_plan_budget(const PlanInput& in, const std::vector<IrGate>& gates_in, Plan& plan,
+                            std::string& err, double wo_budget);
+
+// The write-only first pass (booster / basis source fused) gets an FP64
+// budget (c15): about the work its 16 B/amp of writes hide (~40 FP64/amp).
+// A larger budget can save a whole read/write pass later (QAOA-30: 12 -> 11
+// passes at 64), so the optimiser plans with both and keeps the plan with
+// fewer full-state passes (ties: the balanced 40).  QS_WO_BUDGET pins one.
 int make_plan(const PlanInput& in, const std::vector<IrGate>& gates_in, Plan& plan,
               std::string& err) {
+  const char* e = getenv("QS_WO_BUDGET");  // experiment knob
+  if (e && *e) return make_plan_budget(in, gates_in, plan, err, atof(e));
+  int rc = make_plan_budget(in, gates_in, plan, err, 40.0);
+  if (rc || !in.product_state || plan.stats.n_passes < 3) return rc;
+  Plan alt;
+  std::string err2;
+  if (make_plan_budget(in, gates_in, alt, err2, 64.0) == QS_OK && alt.stats.n_passes < plan.stats.n_passes)
+    plan = std::move(alt);
+  return QS_OK;
+}
+
+static int make_plan_budget(const PlanInput& in, const std::vector<IrGate>& gates_in, Plan& plan,
+                            std::string& err, double wo_budget) {
   plan = Plan();
   plan.n = in.n;
   plan.n_global = in.n_global;
@@ -995,6 +1013,7 @@ int make_plan(const PlanInput& in, const std::vector<IrGate>& gates_in, Plan& pl
   Sched S;
   S.plan = &plan;
   S.cfg = &in.cfg;
+  S.wo_budget = wo_budget;
   std::vector<int> map = in.map;
   std::vector<IrGate> gates = gates_in;
   if (in.product_state) {
