@@ -212,6 +212,7 @@ def cpu_baseline(workload: str, n: int, budget_s: float = 15.0) -> dict:
     host cores), plus a single-thread leg at n = 26."""
     import oracle
     key = "%s%d" % (workload, n)
+    oracle.set_num_threads(os.cpu_count() or 1)
     s = OracleSampler(workload, n)
     r = s.sample(budget_s)
     del s
@@ -251,6 +252,9 @@ def run_reference(args):
     n = args.n or (30 + g)
     key = "%s%d" % (args.workload, n)
     per_step = max(2.0, min(15.0, 150.0 / max(1, args.steps + args.warmup)))
+    # torchrun exports OMP_NUM_THREADS=1: the reference arm runs on all the
+    # host's cores, like the N = 1 leg
+    oracle.set_num_threads(os.cpu_count() or 1)
     s = OracleSampler(args.workload, n)
     for _ in range(args.warmup):
         s.sample(per_step)

@@ -987,17 +987,20 @@ static int make_plan_budget(const PlanInput& in, const std::vector<IrGate>& gate
 // budget (c15): about the work its 16 B/amp of writes hide (~40 FP64/amp).
 // A larger budget can save a whole read/write pass later (QAOA-30: 12 -> 11
 // passes at 64), so the optimiser plans with both and keeps the plan with
-// fewer full-state passes (ties: the balanced 40).  QS_WO_BUDGET pins one.
+// fewer full-state passes (candidates 40, 48, 64; ties: the smaller, more
+// balanced budget).  QS_WO_BUDGET pins one.
 int make_plan(const PlanInput& in, const std::vector<IrGate>& gates_in, Plan& plan,
               std::string& err) {
   const char* e = getenv("QS_WO_BUDGET");  // experiment knob
   if (e && *e) return make_plan_budget(in, gates_in, plan, err, atof(e));
   int rc = make_plan_budget(in, gates_in, plan, err, 40.0);
   if (rc || !in.product_state || plan.stats.n_passes < 3) return rc;
-  Plan alt;
-  std::string err2;
-  if (make_plan_budget(in, gates_in, alt, err2, 64.0) == QS_OK && alt.stats.n_passes < plan.stats.n_passes)
-    plan = std::move(alt);
+  for (double b : {48.0, 64.0}) {
+    Plan alt;
+    std::string err2;
+    if (make_plan_budget(in, gates_in, alt, err2, b) == QS_OK && alt.stats.n_passes < plan.stats.n_passes)
+      plan = std::move(alt);
+  }
   return QS_OK;
 }
 
