@@ -240,32 +240,60 @@ bool table_columns(const unsigned char* blob, TabCols* v, std::map<int, int>* sl
 // low chunk run in doubles.  One cp.async.bulk.tensor per chunk, box = the
 // chunk dims in full and 1 along the others; the smem image is the linear
 // chunk-index layout, like the bulk stage.
+// More runs than 5 dims (round 2): dims 0-3 are the lowest four runs and
+// dim 4 ("rest") spans every higher position with box 1; the chunk positions
+// inside it (`extra`) are enumerated by 2^|extra| <= 32 copies per chunk (one
+// per lane), copy e landing at e * 2^(covered chunk bits) -- still the linear
+// chunk-index layout (chunk bits are numbered by ascending position).
 struct TPlan {
   int rank = 0;
   int pos[5], len[5];
   bool chunk[5];
+  int n_extra = 0;
+  int extra[kChunkBits];     // chunk positions inside the rest dim
+  int covered = kChunkBits;  // chunk bits covered by one copy
 };
 bool tensor_plan(const KPass& h, TPlan* t) {
   if (getenv("QS_JIT_NOTENSOR")) return false;  // A/B knob
+  static const int max_copies = getenv("QS_JIT_TENSOR_COPIES") ? atoi(getenv("QS_JIT_TENSOR_COPIES")) : 32;
   u64 cm = 0;
   for (int c = 0; c < kChunkBits; c++) cm |= 1ull << h.cpos[c];
   int l = 0;
   while (l < kChunkBits && h.cpos[l] == l) l++;
   if (l < 3 || l >= 5) return false;
-  t->rank = 0;
+  std::vector<int> rp, rl;
+  std::vector<bool> rc;
   int p = 0;
   while (p < h.nl) {
     const bool in = (cm >> p) & 1;
     int q = p;
     while (q < h.nl && (((cm >> q) & 1) != 0) == in && (!in || q - p < 8)) q++;
-    if (t->rank == 5) return false;
-    t->pos[t->rank] = p;
-    t->len[t->rank] = q - p;
-    t->chunk[t->rank] = in;
-    t->rank++;
+    rp.push_back(p);
+    rl.push_back(q - p);
+    rc.push_back(in);
     p = q;
   }
-  return t->chunk[0] && t->pos[0] == 0 && t->len[0] == l;
+  if (!rc[0] || rp[0] != 0 || rl[0] != l) return false;
+  t->n_extra = 0;
+  t->covered = kChunkBits;
+  if (rp.size() <= 5) {
+    t->rank = (int)rp.size();
+    for (int d = 0; d < t->rank; d++) t->pos[d] = rp[d], t->len[d] = rl[d], t->chunk[d] = rc[d];
+    return true;
+  }
+  if (max_copies <= 1) return false;
+  t->rank = 5;
+  t->covered = 0;
+  for (int d = 0; d < 4; d++) {
+    t->pos[d] = rp[d], t->len[d] = rl[d], t->chunk[d] = rc[d];
+    if (rc[d]) t->covered += rl[d];
+  }
+  t->pos[4] = rp[4];
+  t->len[4] = h.nl - rp[4];
+  t->chunk[4] = false;
+  for (int q = rp[4]; q < h.nl; q++)
+    if (cm >> q & 1) t->extra[t->n_extra++] = q;
+  return (1 << t->n_extra) <= max_copies && t->len[4] <= 32;
 }
 
 struct Gen {
@@ -1100,18 +1128,29 @@ struct Gen {
     variant = !pipe ? JV_WRITE_ONLY : use_tensor ? JV_TENSOR : use_tma ? JV_BULK : JV_CPASYNC;
     o << "struct __align__(64) QsTmap { u64 v[16]; };\n";
     if (use_tensor) {
-      // one tensor copy per chunk (coordinates: the non-chunk runs' index bits)
+      // one tensor copy per chunk (coordinates: the non-chunk runs' index
+      // bits), or one per lane for the 2^n_extra sub-boxes of the rest dim
+      const int ncopy = 1 << tp.n_extra;
       o << "__device__ __forceinline__ void issue(const double2* __restrict__ state, u64 chunk, double2* dst, u64* bar, u32 lane, const QsTmap* tm) {\n"
         << "  (void)state;\n"
-        << "  if (lane == 0) {\n"
-        << "    const u64 cb = " << cbexpr << ";\n"
-        << "    mbar_expect(bar, " << CH * 16 << "u);\n"
+        << "  if (lane == 0) mbar_expect(bar, " << CH * 16 << "u);\n"
+        << "  __syncwarp();\n"
+        << "  const u64 cb = " << cbexpr << ";\n"
+        << "  for (u32 e = lane; e < " << ncopy << "u; e += 32u) {\n"
         << "    asm volatile(\"cp.async.bulk.tensor." << tp.rank << "d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {";
       for (int d = 0; d < tp.rank; d++) o << (d ? ", " : "") << "%" << d + 2;
-      o << "}], [" << "%" << tp.rank + 2 << "];\"\n      :: \"r\"(sa(dst)), \"l\"(tm)";
+      o << "}], [" << "%" << tp.rank + 2 << "];\"\n      :: \"r\"(sa(dst + e * " << (1 << tp.covered) << "u)), \"l\"(tm)";
       for (int d = 0; d < tp.rank; d++) {
-        if (tp.chunk[d]) o << ", \"r\"(0)";
-        else o << ", \"r\"((u32)((cb >> " << tp.pos[d] << ") & " << ((1ull << tp.len[d]) - 1) << "ull))";
+        if (tp.chunk[d]) {
+          o << ", \"r\"(0)";
+        } else if (d == 4 && tp.n_extra) {
+          o << ", \"r\"((u32)((cb >> " << tp.pos[d] << ") & " << ((1ull << tp.len[d]) - 1) << "ull)";
+          for (int x = 0; x < tp.n_extra; x++)
+            o << " | (((e >> " << x << ") & 1u) << " << tp.extra[x] - tp.pos[4] << ")";
+          o << ")";
+        } else {
+          o << ", \"r\"((u32)((cb >> " << tp.pos[d] << ") & " << ((1ull << tp.len[d]) - 1) << "ull))";
+        }
       }
       o << ", \"r\"(sa(bar)) : \"memory\");\n  }\n  __syncwarp();\n}\n";
     } else if (use_tma) {
