@@ -17,7 +17,7 @@ COLS = {
 STALLS = ["long_scoreboard", "short_scoreboard", "mio_throttle", "barrier", "lg_throttle", "math_pipe_throttle",
           "wait", "not_selected"]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
-         "second": 1.0}
+         "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 
 
 def main(path):
