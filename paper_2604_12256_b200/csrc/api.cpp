@@ -750,6 +750,7 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
             // with QS_JIT_WO_MINB (A/B knob) keep grids a multiple of 8 so the
             // hoisted expand gathers stay enabled at 3 CTAs per SM
             if (getenv("QS_JIT_WO_MINB") && per_sm != 2 && grid > 8) grid &= ~7ull;
+            if (jp.grid_mult > 1 && grid > (u64)jp.grid_mult) grid -= grid % (u64)jp.grid_mult;
             if (grid > h.n_chunks) grid = h.n_chunks;
             const unsigned char* hb = blobs[si].data() + blob_off[si][k];
             const size_t pb = jit_param_bytes(hb);

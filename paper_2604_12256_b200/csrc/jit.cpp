@@ -255,7 +255,7 @@ struct TPlan {
 };
 bool tensor_plan(const KPass& h, TPlan* t) {
   if (getenv("QS_JIT_NOTENSOR")) return false;  // A/B knob
-  static const int max_copies = getenv("QS_JIT_TENSOR_COPIES") ? atoi(getenv("QS_JIT_TENSOR_COPIES")) : 32;
+  static const int max_copies = getenv("QS_JIT_TENSOR_COPIES") ? atoi(getenv("QS_JIT_TENSOR_COPIES")) : 64;
   u64 cm = 0;
   for (int c = 0; c < kChunkBits; c++) cm |= 1ull << h.cpos[c];
   int l = 0;
@@ -402,6 +402,7 @@ struct Gen {
   bool table_free = false;    // generation assumes no table: 4 KB more for hoists
   bool bad_op = false;        // an op type the generator does not know
   int variant = 0;            // chunk refill engine (JitVariant)
+  int grid_mult = 1;          // the grid must be a multiple of this (hoisted expand gathers)
   // Chunk groups per CTA: multi-layout load passes (compute-heavy between
   // their load and their store) run two groups over three buffers so a load
   // is always in flight; the others run one group (two CTAs per SM, one
@@ -1100,7 +1101,7 @@ struct Gen {
             const int pos = h.run_dst[i] + t;
             if (pos >= glo && pos < ghi) b = std::max(b, h.run_src[i] + t + 1);
           }
-        if (b <= 3) xh_g = g, xh_b = b;  // grids are 2 x 148 CTAs = 8 x 37
+        if (b <= 3) xh_g = g, xh_b = b;  // the launcher keeps grids a multiple of 8 (grid_mult)
       }
     }
     const int CH = 1 << kChunkBits;
@@ -1247,7 +1248,11 @@ struct Gen {
         << ");\n  (void)issued;\n";
     hz_off = mbar_off + (pipe ? ((NB * 12 + 15) / 16) * 16 : 0);
     const size_t xh_off = hz_off;
-    if (xh_g >= 0) hz_off += (size_t)kNReg * kThreads * 16;
+    if (xh_g >= 0) {
+      hz_off += (size_t)kNReg * kThreads * 16;
+      static const bool xh_grid = getenv("QS_JIT_XHGRID") == nullptr || atoi(getenv("QS_JIT_XHGRID")) != 0;
+      if (xh_grid) grid_mult = 1 << xh_b;  // e.g. 148 -> 144 CTAs: the gathers stay hoisted
+    }
     // hoisted per-thread values (shared by the groups: they depend on tid only)
     // fill what shared memory is left: 227 KB per CTA (two CTAs per SM: half
     // of 228 KB, less the per-CTA reservation), minus the 4 KB sincos table
@@ -1702,6 +1707,7 @@ struct Compiled {
   int blocks_per_sm = 1;
   size_t smem = 0;
   int variant = 0;
+  int grid_mult = 1;
 };
 
 std::mutex g_mu;
@@ -1767,6 +1773,7 @@ struct Source {
   size_t smem = 0;
   int threads = kThreads;
   int variant = 0;
+  int grid_mult = 1;
   bool ok = false;
 };
 
@@ -1781,6 +1788,7 @@ Source make_source(const unsigned char* blob) {
   r.smem = g.hz_off + (size_t)g.n_hoist * kThreads * 16;
   r.threads = g.nthreads;
   r.variant = g.variant;
+  r.grid_mult = g.grid_mult;
   bool bad = g.bad_op;
   // hoists were capped only by the table's 4 KB: if the extra room takes
   // every loop-invariant sincos out of the loop, no table is needed at all
@@ -1793,6 +1801,7 @@ Source make_source(const unsigned char* blob) {
       r.smem = g2.hz_off + (size_t)g2.n_hoist * kThreads * 16;
       r.threads = g2.nthreads;
       r.variant = g2.variant;
+      r.grid_mult = g2.grid_mult;
       bad = g2.bad_op;
     }
   }
@@ -1878,6 +1887,7 @@ int jit_prepare_all(const std::vector<const unsigned char*>& blobs, int device,
           P.smem = c->second.smem;
           P.threads = c->second.threads;
           P.variant = c->second.variant;
+          P.grid_mult = c->second.grid_mult;
           need[i] = 0;
           continue;
         }
@@ -1990,6 +2000,7 @@ int jit_prepare_all(const std::vector<const unsigned char*>& blobs, int device,
     c.smem = S.smem;
     c.threads = S.threads;
     c.variant = S.variant;
+    c.grid_mult = S.grid_mult;
     g_cache[key] = c;
     g_threads[(void*)c.f] = S.threads;
   }
@@ -2013,6 +2024,7 @@ int jit_prepare_all(const std::vector<const unsigned char*>& blobs, int device,
         P.smem = it->second.smem;
         P.threads = it->second.threads;
         P.variant = it->second.variant;
+        P.grid_mult = it->second.grid_mult;
       }
     }
     bad += !P.ok;

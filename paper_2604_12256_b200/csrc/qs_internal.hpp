@@ -177,6 +177,7 @@ struct JitPrepared {
   int threads = kThreads;
   size_t smem = 0;
   int variant = 0;      // JitVariant
+  int grid_mult = 1;    // launch grid must be a multiple of this
   std::string err;
 };
 
