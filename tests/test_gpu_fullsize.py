@@ -186,3 +186,39 @@ def test_loopback_16_ranks_unfusable_swaps(qs):
     psi, st, info = run(qs, n, gates, ranks=16)
     assert st["n_swaps"] >= 1
     check(psi, n, gates)
+
+
+@pytest.mark.parametrize("jit", [0, 99])
+def test_unit_scaled_ops_and_pass_scales(qs, jit):
+    """Uncontrolled unit-scaled gates (r9: SX, SY, e^{ia} X, e^{ia} (X+iY)-type
+    Paulis) with their scalars folded into the pass scale: products that are
+    real, pure imaginary, an eighth turn and a general phase; controlled
+    copies keep their matrices.  Both kernel paths, against the oracle."""
+    rng = np.random.default_rng(77)
+    n = 20
+    ph = np.exp(1j * 0.7345)
+    gx = np.array([[0, ph], [ph, 0]])                 # e^{ia} X
+    gy = np.array([[0, -1j * ph], [1j * ph, 0]])      # e^{ia} Y
+    circ = []
+    for layer in range(6):
+        for q in range(n):
+            k = int(rng.integers(5))
+            if k == 0:
+                circ.append(W.Gate("SX", (q,)))
+            elif k == 1:
+                circ.append(W.Gate("SY", (q,)))
+            elif k == 2:
+                circ.append(W.Gate("UNITARY", (q,), (), (), gx))
+            elif k == 3:
+                circ.append(W.Gate("UNITARY", (q,), (), (), gy))
+            else:
+                circ.append(W.Gate("SX", (q,), ((q + 3) % n,)))     # controlled: no extraction
+        circ += [W.Gate("CZ", ((q + 1) % n,), (q,)) for q in range(0, n, 2)]
+        circ += [W.Gate("S", (int(rng.integers(n)),)), W.Gate("T", (int(rng.integers(n)),))]
+    s = qs.Simulator(n)
+    s.set_config(qs.make_config(jit_min_qubits=jit))
+    s.set_basis_state(5)
+    s.apply(circ)
+    psi = s.state()
+    s.close()
+    check(psi, n, circ, basis=5)

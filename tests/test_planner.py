@@ -339,3 +339,30 @@ def test_fusion_reaches_four_targets():
     tks = [len(o["tpos"]) for s in plan["steps"] if s["type"] == "pass" for o in s["ops"] if o["t"] == "dense"]
     assert 4 in tks
     assert np.max(np.abs(psi - oracle.apply_circuit(n, gates, x=1))) < 1e-11
+
+
+def test_write_only_budget_candidates():
+    """The optimiser tries FP64 budgets 40/48/64 for the write-only first pass
+    and keeps the plan with the fewest full-state passes: QAOA-30 p=4 takes
+    11 (12 at the balanced 40), QFT stays at 2 at every bench size."""
+    import bench
+    p = qs.plan_json(30, bench.make_circuit("qaoa", 30), basis=5)
+    assert p["stats"]["n_passes"] <= 11
+    for n, r in ((30, 1), (31, 2), (32, 4), (33, 8)):
+        p = qs.plan_json(n, bench.make_circuit("qft", n), n_ranks=r, basis=5)
+        assert p["stats"]["n_passes"] == 2, (n, r)
+
+
+@pytest.mark.parametrize("name", ["SX", "SY"])
+def test_unit_scaled_gates_replay(name):
+    """SX / SY (unit-scaled: +-lam, +-i lam entries) on a 14-qubit state with
+    other gates around: the plan replays to the oracle (the kernels' scalar
+    extraction is covered by the GPU tests)."""
+    n = 14
+    gates = []
+    for q in range(n):
+        gates.append(W.Gate(name, (q,)))
+        gates.append(W.Gate("CZ", ((q + 1) % n,), (q,)))
+    gates += W.random_circuit(n, 40, 3)
+    _, psi = run(n, gates, basis=9)
+    assert np.max(np.abs(psi - oracle.apply_circuit(n, gates, x=9))) < 1e-11
