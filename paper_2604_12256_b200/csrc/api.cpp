@@ -813,9 +813,12 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
   double tswap = 0;
   if (ctx->timing) {
     Shard& s0 = ctx->shards[0];
+    static const bool dump = getenv("QS_TIMING_DUMP") != nullptr;  // per-launch times (diagnostics)
     for (const Timed& t : s0.timed) {
       float ms = 0;
       CU(cudaEventElapsedTime(&ms, t.a, t.b));
+      if (dump) fprintf(stderr, "qs_timing rank %d kind %d ms %.4f bytes %llu\n", s0.rank, t.kind, ms,
+                        (unsigned long long)t.bytes);
       ctx->k_count[t.kind]++;
       ctx->k_ms[t.kind] += ms;
       ctx->k_bytes[t.kind] += t.bytes;

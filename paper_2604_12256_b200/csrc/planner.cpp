@@ -995,7 +995,11 @@ int make_plan(const PlanInput& in, const std::vector<IrGate>& gates_in, Plan& pl
   if (e && *e) return make_plan_budget(in, gates_in, plan, err, atof(e));
   int rc = make_plan_budget(in, gates_in, plan, err, 40.0);
   if (rc || !in.product_state || plan.stats.n_passes < 3) return rc;
+  // (sharded states: 40/48 only -- QAOA-32 on 4 GPUs takes 13 passes at 64
+  // but two of its fused-swap passes then run at half the NVLink rate, 186
+  // vs 150 ms, measured per launch; QFT-32 on 4 GPUs needs 48 for 2 passes)
   for (double b : {48.0, 64.0}) {
+    if (in.n_global > 0 && b > 48.0) break;
     Plan alt;
     std::string err2;
     if (make_plan_budget(in, gates_in, alt, err2, b) == QS_OK && alt.stats.n_passes < plan.stats.n_passes)
