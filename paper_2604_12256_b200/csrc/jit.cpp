@@ -1652,6 +1652,21 @@ struct Gen {
   }
 };
 
+// 64-bit word-wise hash of a descriptor (the memo key; the kernel cache key
+// is fnv1a of the generated source)
+u64 blob_hash(const unsigned char* p, size_t n) {
+  u64 h = 0x9E3779B97F4A7C15ull ^ n;
+  size_t i = 0;
+  for (; i + 8 <= n; i += 8) {
+    u64 w;
+    memcpy(&w, p + i, 8);
+    h = (h ^ w) * 0xff51afd7ed558ccdull;
+    h ^= h >> 29;
+  }
+  for (; i < n; i++) h = (h ^ p[i]) * 1099511628211ull;
+  return h ^ (h >> 31);
+}
+
 u64 fnv1a(const std::string& s) {
   u64 h = 1469598103934665603ull;
   for (unsigned char c : s) {
@@ -1713,7 +1728,11 @@ struct Compiled {
 std::mutex g_mu;
 std::unordered_map<u64, Compiled> g_cache;  // key: hash ^ device
 std::unordered_map<void*, int> g_threads;   // function -> threads per CTA
-std::unordered_map<u64, u64> g_blob_src;    // descriptor bytes hash -> source hash
+struct BlobMemo {
+  std::vector<unsigned char> bytes;  // the descriptor (a hit compares it in full)
+  u64 src_hash = 0;
+};
+std::unordered_map<u64, BlobMemo> g_blob_src;  // descriptor hash -> source hash
 double g_compile_ms = 0;
 uint64_t g_compiles = 0, g_disk_hits = 0;
 
@@ -1875,10 +1894,11 @@ int jit_prepare_all(const std::vector<const unsigned char*>& blobs, int device,
     for (size_t i = 0; i < n; i++) {
       KPass hh;
       memcpy(&hh, blobs[i], sizeof hh);
-      bh[i] = fnv1a(std::string(reinterpret_cast<const char*>(blobs[i]), hh.total_bytes));
+      bh[i] = blob_hash(blobs[i], hh.total_bytes);
       auto it = g_blob_src.find(bh[i]);
-      if (!compile_only && it != g_blob_src.end()) {
-        auto c = g_cache.find(it->second ^ ((u64)(device + 1) * 0x9E3779B97F4A7C15ull));
+      if (!compile_only && it != g_blob_src.end() && it->second.bytes.size() == hh.total_bytes &&
+          memcmp(it->second.bytes.data(), blobs[i], hh.total_bytes) == 0) {
+        auto c = g_cache.find(it->second.src_hash ^ ((u64)(device + 1) * 0x9E3779B97F4A7C15ull));
         if (c != g_cache.end()) {
           JitPrepared& P = out[i];
           P.ok = true;
@@ -1904,7 +1924,13 @@ int jit_prepare_all(const std::vector<const unsigned char*>& blobs, int device,
   {
     std::lock_guard<std::mutex> lk(g_mu);
     for (size_t i : todo)
-      if (srcs[i].ok) g_blob_src[bh[i]] = srcs[i].hash;
+      if (srcs[i].ok) {
+        KPass hh;
+        memcpy(&hh, blobs[i], sizeof hh);
+        BlobMemo& m = g_blob_src[bh[i]];
+        m.bytes.assign(blobs[i], blobs[i] + hh.total_bytes);
+        m.src_hash = srcs[i].hash;
+      }
   }
   // unique sources that are not loaded on this device yet
   std::map<u64, size_t> uniq;  // hash -> first pass index
