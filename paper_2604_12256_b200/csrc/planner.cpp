@@ -294,6 +294,12 @@ static std::vector<cd> fuse_pair(const POp& a, const POp& b, std::vector<int>& u
 
 static void fuse_ops(std::vector<POp>& ops, int fuse_cap) {
   if (fuse_cap < 2) return;
+  // Fusion must make the op strictly cheaper: at equal FP64 cost (e.g. RX x
+  // RX: 8 = 4 + 4 per amplitude) the fused 4x4 needs 16 matrix constants
+  // instead of 2 x 4, which the compiler keeps in registers (spills in
+  // QAOA's write-only pass).  QS_FUSE_TIES=1: the round-1 rule (ties fuse).
+  static const bool ties = getenv("QS_FUSE_TIES") != nullptr;
+  auto pays = [](double fused, double parts) { return ties ? fused <= parts : fused < parts; };
   const int cap = std::min(fuse_cap, kRegBits);          // run fusion
   const int pcap = std::min(fuse_cap, kRegBits - 1);     // pairwise (register ops)
   auto fusable = [](const POp& o) { return o.type == POp::DENSE && o.cmask == 0 && (int)o.tpos.size() < kRegBits; };
@@ -321,7 +327,7 @@ static void fuse_ops(std::vector<POp>& ops, int fuse_cap) {
           f.tpos = uni;
           f.n_src += ops[q].n_src;
         }
-        if (mat_cost_unc(f.mat) * (f.tpos.size() >= (size_t)kRegBits ? 2.0 : 1.0) <= parts) {
+        if (pays(mat_cost_unc(f.mat) * (f.tpos.size() >= (size_t)kRegBits ? 2.0 : 1.0), parts)) {
           f.is_h = f.is_x = false;
           out.push_back(std::move(f));
           i = j;
@@ -340,7 +346,7 @@ static void fuse_ops(std::vector<POp>& ops, int fuse_cap) {
       if (ku <= pcap && dense_cost(ku) / 2 <= parts) {
         std::vector<int> uni;
         std::vector<cd> F = fuse_pair(prev, op, uni);
-        if (mat_cost_unc(F) <= parts) {
+        if (pays(mat_cost_unc(F), parts)) {
           prev.mat = F;
           prev.tpos = uni;
           prev.is_h = prev.is_x = false;

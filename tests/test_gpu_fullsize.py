@@ -152,7 +152,7 @@ def test_fused_four_qubit_unitary_n22(qs):
     n = 22
     qb = [1, 9, 14, 20]
     gates = W.random_circuit(n, 20, 3)
-    for _ in range(12):
+    for _ in range(20):
         a, b = (int(x) for x in rng.choice(qb, 2, replace=False))
         gates.append(W.Gate("UNITARY", (a, b), (), (), W.haar_unitary(4, rng)))
     psi, _, _ = run(qs, n, gates, basis=3)

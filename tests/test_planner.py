@@ -332,7 +332,7 @@ def test_fusion_reaches_four_targets():
     n = 16
     qb = [3, 5, 8, 12]
     gates = []
-    for _ in range(12):
+    for _ in range(20):
         a, b = (int(x) for x in rng.choice(qb, 2, replace=False))
         gates.append(W.Gate("UNITARY", (a, b), (), (), W.haar_unitary(4, rng)))
     plan, psi = run(n, gates, basis=1)
