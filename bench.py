@@ -370,7 +370,7 @@ def main():
         plan_ms += st["t_plan_ms"]
         dev_ms += st["t_device_ms"]
         for k in ("K1_chunk", "K2_dense", "K3_diag", "small", "K5_expand", "K5_merge", "init", "K4_swap",
-                  "substate", "fused_swap_pass"):
+                  "substate", "fused_swap_pass", "pull_pass"):
             t = sim.kernel_timing(k)
             a = kt.setdefault(k, {"launches": 0, "ms": 0.0, "bytes": 0})
             for f in a:
@@ -393,7 +393,11 @@ def main():
     nvl = None
     if world > 1 and st["n_swaps"]:
         sw = kt.get("K4_swap", {"ms": 0.0, "launches": 0})
-        fp = kt.get("fused_swap_pass", {"ms": 0.0, "launches": 0})
+        fp = dict(kt.get("fused_swap_pass", {"ms": 0.0, "launches": 0, "bytes": 0}))
+        pp = kt.get("pull_pass", {"ms": 0.0, "launches": 0, "bytes": 0})
+        # a split swap's exchange is spread over the exporting pass and the
+        # pass after it (push/pull): both carry NVLink traffic
+        fp = {k2: fp.get(k2, 0) + pp.get(k2, 0) for k2 in ("ms", "launches", "bytes")}
         unf = st["n_swaps"] - st["n_fused_swaps"]
         per_swap = st["bytes_nvlink"] / st["n_swaps"]   # (1 - 2^-j) x shard bytes per swap (equal j here)
         nvl = {"bytes_per_gpu_per_step": st["bytes_nvlink"], "swaps": st["n_swaps"],

@@ -253,9 +253,12 @@ enum qs_kernel_id {
   QS_K4_SWAP = 7,   /* global<->local exchange                            */
   QS_K6_READ = 8,
   QS_K_SUBSTATE = 9, /* any pass on a booster sub-state (K1/K2/K3/SMALL)  */
-  QS_K1_FUSED_SWAP = 10 /* full-state pass that also performs the following
-                           swap's exchange by NVLink peer stores (f1):
-                           its time covers the pass AND the transfer        */
+  QS_K1_FUSED_SWAP = 10, /* full-state pass that also performs the following
+                            swap's exchange by NVLink peer stores (f1):
+                            its time covers the pass AND the transfer       */
+  QS_K1_PULL = 11        /* the pass after a split fused swap: it loads the
+                            half the exporting pass left in place from the
+                            source ranks' buffers (NVLink reads)            */
 };
 int qs_set_timing(qs_ctx *ctx, int enable);
 /* The cudaStream_t (as void*) the handle launches local shard `i` on, so a

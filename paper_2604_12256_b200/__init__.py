@@ -38,7 +38,7 @@ KINDS = {
 }
 KERNELS = {"K1_chunk": 0, "K2_dense": 1, "K3_diag": 2, "small": 3, "K5_expand": 4,
            "K5_merge": 5, "init": 6, "K4_swap": 7, "K6_read": 8, "substate": 9,
-           "fused_swap_pass": 10}
+           "fused_swap_pass": 10, "pull_pass": 11}
 
 
 class QSError(RuntimeError):

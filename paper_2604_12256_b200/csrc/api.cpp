@@ -565,8 +565,9 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
   bool fuse_vote = true;
   if (any_fusable && ctx->mode == M_RANK && ctx->n_ranks > 1) {
     double v = 1.0;
-    for (size_t k = 0; k + 1 < plan.steps.size(); k++)
-      if (plan.steps[k].type == Step::PASS && plan.steps[k].pass.x_j && !step_jit[k]) v = 0.0;
+    for (size_t k = 0; k < plan.steps.size(); k++)
+      if (plan.steps[k].type == Step::PASS && (plan.steps[k].pass.x_j || plan.steps[k].pass.pull_j) && !step_jit[k])
+        v = 0.0;
     Shard& sh = ctx->shards[0];
     CU(cudaSetDevice(sh.device));
     double* dv = reinterpret_cast<double*>(sh.bar) + 1;
@@ -580,9 +581,14 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
     if (k + 1 >= plan.steps.size()) return false;
     const Step& st = plan.steps[k];
     const Step& nx = plan.steps[k + 1];
+    // a split exporting pass leaves half its chunks for the next pass to
+    // pull: that pass must run its specialised kernel too
+    const bool split_ok = st.type != Step::PASS || st.pass.x_split < 0 ||
+                          (k + 2 < plan.steps.size() && step_jit[k + 2]);
     return st.type == Step::PASS && st.pass.x_j && nx.type == Step::SWAP && nx.fusable && fuse_vote &&
-           step_jit[k] && ensure_peers(ctx) == 1;
+           step_jit[k] && split_ok && ensure_peers(ctx) == 1;
   };
+  std::vector<char> pulling(plan.steps.size(), 0);  // pull pass whose source was split
   ctx->prep_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count();
   for (Shard& sh : ctx->shards) {
     CU(cudaSetDevice(sh.device));
@@ -655,6 +661,7 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
     if (fuse) {
       rc = shard_barrier(ctx);
       if (rc) return rc;
+      if (st.pass.x_split >= 0) pulling[k + 2] = 1;
     }
     for (size_t si = 0; si < ctx->shards.size(); si++) {
       Shard& sh = ctx->shards[si];
@@ -735,11 +742,18 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
           // same way on every shard and rank: plan, kernel readiness vote,
           // collective peer setup); otherwise every destination is our own
           // buffer at our own index
-          u64 xp[1 << kMaxXBits];
-          for (int s = 0; s < (1 << kMaxXBits); s++) xp[s] = (u64)buf;
+          u64 xp[2 << kMaxXBits];
+          for (int s = 0; s < (2 << kMaxXBits); s++) xp[s] = (u64)buf;
           if (fuse) {
             fused_targets(ctx, plan.steps[k + 1], sh.rank, xp);
             ctx->fused_pending = true;
+          }
+          if (pulling[k]) {
+            // pull pass: elements of chunks with the split bit set come from
+            // the buffer the exporting pass left them in, at the source rank
+            // of their piece (the swap's formula with the roles of the two
+            // allocations exchanged: recv_buffer is now each rank's old state)
+            fused_targets(ctx, plan.steps[k - 1], sh.rank, xp + (1 << kMaxXBits));
           }
           const JitPrepared& jp = prep[si][k];
           if (jp.ok) {
@@ -777,7 +791,7 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
             CU(launch_pass(p.kernel, dblob, h, buf, sh.stream));
           }
           ctx->launches++;
-          kind = (p.buf != 0) ? KK_SUB : fuse ? KK_XPASS : p.kernel;  // full-state passes only per kernel
+          kind = (p.buf != 0) ? KK_SUB : fuse ? KK_XPASS : pulling[k] ? KK_PULL : p.kernel;
           bytes = ((p.src_mode ? 16ull : 32ull) << p.nl);
           break;
         }
@@ -788,6 +802,11 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
         CU(cudaEventRecord(b, sh.stream));
         sh.timed.push_back({kind, a, b, bytes});
       }
+    }
+    // nobody may overwrite a buffer another rank is still pulling from
+    if (pulling[k]) {
+      rc = shard_barrier(ctx);
+      if (rc) return rc;
     }
   }
   for (Shard& sh : ctx->shards) {

@@ -1124,10 +1124,23 @@ struct Gen {
     // A/B with QS_JIT_TMA_L=3, QAOA-30 155 ms vs 90 ms, rand30 587 vs 333 ms)
     static const int tma_min_l = getenv("QS_JIT_TMA_L") ? atoi(getenv("QS_JIT_TMA_L")) : 5;  // A/B knob
     TPlan tp;
-    const bool use_tensor = pipe && l < tma_min_l && low_run(L[0]) <= 1 && tensor_plan(h, &tp);
+    const bool pull = h.pull_j > 0;
+    const bool use_tensor = pipe && !pull && l < tma_min_l && low_run(L[0]) <= 1 && tensor_plan(h, &tp);
     const bool use_tma = (pipe && l >= tma_min_l && low_run(L[0]) <= 1 && !getenv("QS_JIT_NOTMA")) || use_tensor;
     variant = !pipe ? JV_WRITE_ONLY : use_tensor ? JV_TENSOR : use_tma ? JV_BULK : JV_CPASYNC;
     o << "struct __align__(64) QsTmap { u64 v[16]; };\n";
+    // buffer table (kernel parameter xp, copied to shared memory once: a
+    // dynamically indexed parameter would be copied to local memory)
+    if (pull || h.x_mask) o << "__shared__ u64 qs_ptab[16];\n";
+    if (pull) {
+      // pull pass: the buffer an element is read from -- table entry
+      // (z << 3) | piece, piece = its bits at the swap's local positions
+      o << ""
+        << "__device__ __forceinline__ const double2* pull_src(u64 idx) {\n"
+        << "  const u32 e = (u32)(((idx >> " << (int)h.pull_z << ") & 1ull) << 3)";
+      for (int t = 0; t < h.pull_j; t++) o << " | (u32)(((idx >> " << (int)h.pull_pos[t] << ") & 1ull) << " << t << ")";
+      o << ";\n  return reinterpret_cast<const double2*>(qs_ptab[e]);\n}\n";
+    }
     if (use_tensor) {
       // one tensor copy per chunk (coordinates: the non-chunk runs' index
       // bits), or one per lane for the 2^n_extra sub-boxes of the rest dim
@@ -1164,7 +1177,8 @@ struct Gen {
         << "    const u64 off = 0ull";
       for (int i = 0; i < kChunkBits - l; i++)
         o << " | ((u64)((seg >> " << i << ") & 1) << " << (int)h.cpos[l + i] << ")";
-      o << ";\n    bulk_g2s(dst + (seg << " << l << "), state + (cb | off), " << (16 << l) << "u, bar);\n"
+      o << ";\n    bulk_g2s(dst + (seg << " << l << "), " << (pull ? "pull_src(cb | off)" : "state") << " + (cb | off), "
+        << (16 << l) << "u, bar);\n"
         << "  }\n}\n";
     } else if (pipe) {
       // thread t copies chunk elements c = t + 256 i (coalesced 128 B+ runs)
@@ -1176,7 +1190,11 @@ struct Gen {
         u64 off = 0;
         for (int k = 0; k < kRegBits; k++)
           if (i >> k & 1) off |= 1ull << h.cpos[kLogT + k];
-        o << "  cp_async16(stage + (sd ^ " << host_swz(i << kLogT) << "), sp + " << u(off) << ");\n";
+        if (pull)
+          o << "  cp_async16(stage + (sd ^ " << host_swz(i << kLogT) << "), pull_src(cb | tpd | " << u(off) << ") + (cb | tpd | "
+            << u(off) << "));\n";
+        else
+          o << "  cp_async16(stage + (sd ^ " << host_swz(i << kLogT) << "), sp + " << u(off) << ");\n";
       }
       o << "  cp_async_mbar_arrive(bar);\n}\n";
     }
@@ -1217,7 +1235,7 @@ struct Gen {
     if (param_pool) o << "struct QsPool { double v[" << npool << "]; };\n";
     // fused swap: destination base per value of the exported
     // top local bits (receive buffers of this rank or its peers, by value)
-    o << "struct QsXPeer { u64 v[8]; };\n";
+    o << "struct QsXPeer { u64 v[16]; };\n";
     // QS_JIT_WO_MINB: A/B knob for the resident-CTA target of one-group passes
     static const int wo_minb = getenv("QS_JIT_WO_MINB") ? atoi(getenv("QS_JIT_WO_MINB")) : 2;
     o << "extern \"C\" __global__ void __launch_bounds__(" << nthreads << ", " << (NG == 1 && NB <= 1 ? wo_minb : 1)
@@ -1281,6 +1299,11 @@ struct Gen {
         << "    for (int b = 0; b < " << NB << "; b++) { mbar_init(mbar + b, " << (use_tma ? 1 : kThreads)
         << "); issued[b] = 0u; }\n"
         << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n  }\n";
+    }
+    if (pull || h.x_mask) {
+      o << "  if (threadIdx.x == 0) {\n";
+      for (int i = 0; i < 16; i++) o << "    qs_ptab[" << i << "] = xp.v[" << i << "];\n";
+      o << "  }\n";
     }
     o << "  __syncthreads();\n";
     if (use_tma) {
@@ -1594,6 +1617,14 @@ struct Gen {
       // come from the chunk index, the thread or the register (disjoint bits)
       int xj = 0;
       while ((1 << xj) <= h.x_mask) xj++;
+      if (h.x_split >= 0) {
+        // push/pull split: chunks with bit x_split set stay in place (the
+        // pass after the swap pulls them from this buffer)
+        o << "    if ((cb >> " << (int)h.x_split << ") & 1ull) { double2* __restrict__ so = state + (cb | tpo);\n";
+        for (int r = 0; r < kNReg; r++)
+          o << "      so[" << u(reg_phys(nlay - 1, r, true)) << "] = " << A(r) << ";\n";
+        o << "    } else\n";
+      }
       o << "    { const u64 xi = cb | tpo;\n      const u32 sct = 0u";
       for (int i = 0; i < xj; i++) o << " | ((u32)((xi >> " << (int)h.x_pos[i] << ") & 1ull) << " << i << ")";
       o << ";\n";
@@ -1601,7 +1632,7 @@ struct Gen {
         const u64 ro = reg_phys(nlay - 1, r, true);
         u64 sr = 0;
         for (int i = 0; i < xj; i++) sr |= ((ro >> h.x_pos[i]) & 1ull) << i;
-        o << "      reinterpret_cast<double2*>(xp.v[sct | " << sr << "u])[xi + " << u(ro) << "] = " << A(r)
+        o << "      reinterpret_cast<double2*>(qs_ptab[sct | " << sr << "u])[xi + " << u(ro) << "] = " << A(r)
           << ";\n";
       }
       o << "    }\n";
@@ -2100,7 +2131,7 @@ bool jit_tensor_map(const unsigned char* blob, const void* state, void* out128) 
   while (l < kChunkBits && h.cpos[l] == l) l++;
   TPlan tp;
   if (h.src_mode != 0 || h.kernel == KK_SMALL || l >= tma_min_l || Gen::low_run(h.phases[0]) > 1 ||
-      !tensor_plan(h, &tp))
+      h.pull_j > 0 || !tensor_plan(h, &tp))
     return false;
   Driver& d = driver();
   if (!d.tmap) return false;
@@ -2130,7 +2161,8 @@ cudaError_t jit_launch(void* fn, int grid, size_t smem, const unsigned char* dbl
     auto it = g_threads.find(fn);
     if (it != g_threads.end()) threads = it->second;
   }
-  u64 xp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  u64 xp[16];
+  memset(xp, 0, sizeof xp);
   if (xpeer8) memcpy(xp, xpeer8, sizeof xp);
   void* args[] = {(void*)&dblob, (void*)&state, (void*)&rank_base, (void*)&vtab, (void*)xp,
                   (void*)tm, (void*)pool_host};

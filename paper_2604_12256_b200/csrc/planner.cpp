@@ -988,6 +988,7 @@ static int booster(Sched& S, int n, std::vector<IrGate>& gates, std::string& err
 // ------------------------------------------------------------ make_plan
 static int make_plan_budget(const PlanInput& in, const std::vector<IrGate>& gates_in, Plan& plan,
                             std::string& err, double wo_budget);
+static void mark_pull_splits(Plan& plan, const qs_config_t& cfg);
 
 // The write-only first pass (booster / basis source fused) gets an FP64
 // budget (c15): about the work its 16 B/amp of writes hide (~40 FP64/amp).
@@ -998,9 +999,17 @@ static int make_plan_budget(const PlanInput& in, const std::vector<IrGate>& gate
 int make_plan(const PlanInput& in, const std::vector<IrGate>& gates_in, Plan& plan,
               std::string& err) {
   const char* e = getenv("QS_WO_BUDGET");  // experiment knob
-  if (e && *e) return make_plan_budget(in, gates_in, plan, err, atof(e));
+  if (e && *e) {
+    const int rc = make_plan_budget(in, gates_in, plan, err, atof(e));
+    if (rc == QS_OK) mark_pull_splits(plan, in.cfg);
+    return rc;
+  }
   int rc = make_plan_budget(in, gates_in, plan, err, 40.0);
-  if (rc || !in.product_state || plan.stats.n_passes < 3) return rc;
+  if (rc) return rc;
+  if (!in.product_state || plan.stats.n_passes < 3) {
+    mark_pull_splits(plan, in.cfg);
+    return QS_OK;
+  }
   // (sharded states: 40/48 only -- QAOA-32 on 4 GPUs takes 13 passes at 64
   // but two of its fused-swap passes then run at half the NVLink rate, 186
   // vs 150 ms, measured per launch; QFT-32 on 4 GPUs needs 48 for 2 passes)
@@ -1011,6 +1020,7 @@ int make_plan(const PlanInput& in, const std::vector<IrGate>& gates_in, Plan& pl
     if (make_plan_budget(in, gates_in, alt, err2, b) == QS_OK && alt.stats.n_passes < plan.stats.n_passes)
       plan = std::move(alt);
   }
+  mark_pull_splits(plan, in.cfg);
   return QS_OK;
 }
 
@@ -1050,6 +1060,48 @@ static int make_plan_budget(const PlanInput& in, const std::vector<IrGate>& gate
   if (S.src_mode) flush_source(S);  // circuit left nothing to fuse the source into
   plan.map_out = map;
   return QS_OK;
+}
+
+// Push/pull split of fused swaps.  A fused pass is
+// NVLink-bound: it exports (1 - 2^-j) of the shard while it streams only
+// 32 B/amp through HBM.  When the pass after the swap is a full-state
+// specialised pass and a free split position z is a chunk-id bit of both
+// passes, the exporting pass pushes the chunks with z = 0 and leaves the
+// z = 1 chunks in place; the next pass loads those elements straight from
+// the source ranks' buffers (NVLink reads; the source of an element is its
+// piece = its bits at the swap's local positions), so both passes carry half
+// the link traffic.  Data placement after the next pass is unchanged.
+static void mark_pull_splits(Plan& plan, const qs_config_t& cfg) {
+  if (plan.n_global == 0 || getenv("QS_NO_PULL")) return;
+  for (size_t i = 0; i + 2 < plan.steps.size(); i++) {
+    Step& a = plan.steps[i];
+    Step& sw = plan.steps[i + 1];
+    Step& b = plan.steps[i + 2];
+    if (a.type != Step::PASS || sw.type != Step::SWAP || !sw.fusable || b.type != Step::PASS) continue;
+    PassPlan& pk = a.pass;
+    PassPlan& pn = b.pass;
+    if (pk.buf != 0 || pn.buf != 0 || pk.x_j == 0 || pn.kernel == KK_SMALL || pn.src_mode != 0 ||
+        pn.nl < cfg.jit_min_qubits || pn.x_j)
+      continue;
+    u64 ck = 0, cn = 0, lp = 0;
+    for (int c : pk.cpos) ck |= 1ull << c;
+    for (int c : pn.cpos) cn |= 1ull << c;
+    for (int q : sw.lpos) lp |= 1ull << q;
+    // the pull pass loads each element from the buffer its piece (bits at
+    // lpos, usually chunk bits: the swap brings in the qubits it acts on)
+    // selects; a contiguous low run of the chunk must not straddle pieces
+    int l = 0;
+    while (l < (int)pn.cpos.size() && pn.cpos[l] == l) l++;
+    if (lp & ((1ull << l) - 1)) continue;
+    int z = -1;
+    for (int q = pk.nl - 1; q >= 0 && z < 0; q--)
+      if (!(ck >> q & 1) && !(cn >> q & 1) && !(lp >> q & 1)) z = q;
+    if (z < 0) continue;
+    pk.x_split = z;
+    pn.pull_j = sw.j;
+    pn.pull_z = z;
+    pn.pull_pos = sw.lpos;
+  }
 }
 
 // ------------------------------------------------------------ encoding
@@ -1096,6 +1148,14 @@ int encode_pass(const PassPlan& p, int rank, std::vector<unsigned char>& out, st
   cd lam_total(1.0, 0.0);  // scalars factored out of unit-scaled ops
   if (p.x_j < 0 || p.x_j > kMaxXBits) {
     err = "internal: fused swap exports more than 3 qubits";
+    return QS_EINVAL;
+  }
+  h.x_split = (int8_t)p.x_split;
+  h.pull_j = (int8_t)p.pull_j;
+  h.pull_z = (int8_t)p.pull_z;
+  for (int i = 0; i < 5; i++) h.pull_pos[i] = (int8_t)(i < (int)p.pull_pos.size() ? p.pull_pos[i] : 0);
+  if (p.pull_j > kMaxXBits) {
+    err = "internal: pull of more than 3 qubits";
     return QS_EINVAL;
   }
   h.x_shift = p.x_j ? p.nl - p.x_j : 0;
@@ -1543,6 +1603,7 @@ std::string plan_to_json(const Plan& plan, bool detail) {
         const PassPlan& p = st.pass;
         o << "\"type\":\"pass\",\"kernel\":\"" << kname(p.kernel) << "\",\"buf\":" << p.buf
           << ",\"nl\":" << p.nl << ",\"src_mode\":" << p.src_mode << ",\"x_j\":" << p.x_j
+          << ",\"x_split\":" << p.x_split << ",\"pull_j\":" << p.pull_j << ",\"pull_z\":" << p.pull_z
           << ",\"x_pos\":[" << (p.x_j > 0 ? std::to_string(p.x_pos[0]) : "")
           << (p.x_j > 1 ? "," + std::to_string(p.x_pos[1]) : "") << (p.x_j > 2 ? "," + std::to_string(p.x_pos[2]) : "")
           << "]"

@@ -61,6 +61,14 @@ struct PassPlan {
   // receive buffer of the rank the swap sends piece s to (0: not fused)
   int x_j = 0;
   std::vector<int> x_pos;     // the swap's local positions (exported bit i)
+  // push/pull split of a fused swap (NVLink time spread over two passes):
+  // the exporting pass pushes only the chunks whose bit `x_split` is 0 (the
+  // rest stay in place, -1: push all); the pass after the swap pulls those
+  // from the source ranks' buffers (pull_j > 0: piece = its bits at
+  // pull_pos, pull_z the split bit)
+  int x_split = -1;
+  int pull_j = 0, pull_z = -1;
+  std::vector<int> pull_pos;
   // filled by encode_pass
   std::vector<std::vector<int>> phase_regs;  // per phase: chunk bits held in registers
   std::vector<int> op_phase;

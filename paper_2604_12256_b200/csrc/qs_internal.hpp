@@ -40,7 +40,9 @@ enum KernelKind {
   KK_SUB = 9,     // passes on booster sub-states (timing class only)
   KK_XPASS = 10,  // full-state pass that also performs the next swap's
                   // exchange by NVLink peer stores (f1; timing class only)
-  KK_NUM = 11
+  KK_PULL = 11,   // full-state pass that loads the other half of a split
+                  // swap from the source ranks' buffers (timing class only)
+  KK_NUM = 12
 };
 
 // Register-op types inside a pass.
@@ -135,6 +137,9 @@ struct KPass {
                        // of unit-scaled dense ops (encode_pass)
   int32_t x_shift, x_mask;  // fused swap export: x_mask = 2^j - 1 (0: none)
   int8_t x_pos[8];          // piece s = sum_i bit x_pos[i] of the local index << i
+  int8_t x_split;           // push only chunks whose bit x_split is 0 (-1: all)
+  int8_t pull_j, pull_z;    // pull pass: source table entry (z << 3) | piece
+  int8_t pull_pos[5];       //   piece = sum_i bit pull_pos[i] << i
   int8_t cpos[16];     // physical position of chunk bit c (loads, ops)
   int8_t opos[16];     // physical position of chunk bit c (stores; relabel)
   int8_t run_src[kMaxRuns], run_dst[kMaxRuns], run_len[kMaxRuns];
