@@ -1010,11 +1010,12 @@ int make_plan(const PlanInput& in, const std::vector<IrGate>& gates_in, Plan& pl
     mark_pull_splits(plan, in.cfg);
     return QS_OK;
   }
-  // (sharded states: 40/48 only -- QAOA-32 on 4 GPUs takes 13 passes at 64
-  // but two of its fused-swap passes then run at half the NVLink rate, 186
-  // vs 150 ms, measured per launch; QFT-32 on 4 GPUs needs 48 for 2 passes)
+  // (more than 2 ranks: 40/48 only -- QAOA-32 on 4 GPUs takes 13 passes at
+  // 64 but two of its fused-swap passes then run at half the NVLink rate:
+  // 160.6 vs 135.7 ms with push/pull, measured per launch; on 2 GPUs the
+  // 64-plan wins, 111.8 vs 116.2 ms.  QFT-32 on 4 GPUs needs 48 for 2 passes)
   for (double b : {48.0, 64.0}) {
-    if (in.n_global > 0 && b > 48.0) break;
+    if (in.n_global > 1 && b > 48.0) break;
     Plan alt;
     std::string err2;
     if (make_plan_budget(in, gates_in, alt, err2, b) == QS_OK && alt.stats.n_passes < plan.stats.n_passes)
