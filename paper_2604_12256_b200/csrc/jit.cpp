@@ -1126,7 +1126,9 @@ struct Gen {
     TPlan tp;
     const bool pull = h.pull_j > 0;
     const bool use_tensor = pipe && !pull && l < tma_min_l && low_run(L[0]) <= 1 && tensor_plan(h, &tp);
-    const bool use_tma = (pipe && l >= tma_min_l && low_run(L[0]) <= 1 && !getenv("QS_JIT_NOTMA")) || use_tensor;
+    static const bool pull_cpa = getenv("QS_JIT_PULL_CPASYNC") != nullptr;  // A/B knob: remote loads per thread
+    const bool use_tma = (pipe && l >= tma_min_l && low_run(L[0]) <= 1 && !getenv("QS_JIT_NOTMA") &&
+                          !(pull && pull_cpa)) || use_tensor;
     variant = !pipe ? JV_WRITE_ONLY : use_tensor ? JV_TENSOR : use_tma ? JV_BULK : JV_CPASYNC;
     o << "struct __align__(64) QsTmap { u64 v[16]; };\n";
     // buffer table (kernel parameter xp, copied to shared memory once: a
