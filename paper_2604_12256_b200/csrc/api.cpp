@@ -102,6 +102,8 @@ struct Shard {
   int8_t* dmap = nullptr;            // logical->physical map (device)
   u64* vtab = nullptr;               // per-chunk shape sums of the running pass
   size_t vtab_cap = 0;               // entries
+  cudaStream_t side = nullptr;       // per-chunk tables of all passes, computed
+                                     // ahead of their passes (overlapping them)
   double2* alloc[2] = {nullptr, nullptr};  // the two shard allocations (state,
                                            // scratch at creation; they alternate)
   double* bar = nullptr;             // rank mode: 1-element all-reduce = barrier
@@ -596,6 +598,52 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
     sh.ev_used = 0;
     CU(cudaEventRecord(sh.t0, sh.stream));
   }
+  // Per-chunk tables (qs_kshape_table) depend only on the descriptors: all
+  // of them are computed on a side stream right at the start, so they
+  // overlap the passes before theirs instead of sitting in front of them
+  // (<= 1 GiB of tables per shard; else each is computed before its pass).
+  std::vector<std::vector<size_t>> tab_off(ctx->shards.size(), std::vector<size_t>(plan.steps.size(), (size_t)-1));
+  std::vector<std::vector<cudaEvent_t>> tab_ev(ctx->shards.size(), std::vector<cudaEvent_t>(plan.steps.size(), nullptr));
+  for (size_t si = 0; si < ctx->shards.size(); si++) {
+    Shard& sh = ctx->shards[si];
+    size_t total = 0;
+    std::vector<TabCols> cols(plan.steps.size());
+    for (size_t k = 0; k < plan.steps.size(); k++) {
+      if (!prep[si][k].ok) continue;
+      const unsigned char* hb = blobs[si].data() + blob_off[si][k];
+      if (!jit_table_cols(hb, &cols[k])) continue;
+      KPass h;
+      memcpy(&h, hb, sizeof h);
+      tab_off[si][k] = total;
+      total += ((size_t)h.n_chunks * cols[k].width + 31) & ~(size_t)31;
+    }
+    if (total == 0) continue;
+    if (total * sizeof(u64) > ((size_t)1 << 30)) {  // too much: tables per pass
+      for (size_t k = 0; k < plan.steps.size(); k++) tab_off[si][k] = (size_t)-1;
+      continue;
+    }
+    CU(cudaSetDevice(sh.device));
+    if (!sh.side) CU(cudaStreamCreateWithFlags(&sh.side, cudaStreamNonBlocking));
+    if (total > sh.vtab_cap) {
+      if (sh.vtab) CU(cudaFree(sh.vtab));
+      sh.vtab = nullptr;
+      sh.vtab_cap = 0;
+      CU(cudaMalloc(&sh.vtab, total * sizeof(u64)));
+      sh.vtab_cap = total;
+    }
+    CU(cudaStreamWaitEvent(sh.side, sh.t0, 0));
+    for (size_t k = 0; k < plan.steps.size(); k++) {
+      if (tab_off[si][k] == (size_t)-1) continue;
+      const unsigned char* hb = blobs[si].data() + blob_off[si][k];
+      KPass h;
+      memcpy(&h, hb, sizeof h);
+      CU(launch_shape_table(sh.arena + blob_off[si][k], sh.vtab + tab_off[si][k], h.rank_base, h.n_chunks, cols[k],
+                            sh.side));
+      ctx->launches++;
+      tab_ev[si][k] = get_event(sh);
+      CU(cudaEventRecord(tab_ev[si][k], sh.side));
+    }
+  }
   const size_t shard_amps = (size_t)1 << ctx->nl;
   for (size_t k = 0; k < plan.steps.size(); k++) {
     const Step& st = plan.steps[k];
@@ -769,7 +817,11 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
             const unsigned char* hb = blobs[si].data() + blob_off[si][k];
             const size_t pb = jit_param_bytes(hb);
             TabCols vl;
-            if (jit_table_cols(hb, &vl)) {
+            u64* vtab = sh.vtab;
+            if (tab_off[si][k] != (size_t)-1) {
+              vtab = sh.vtab + tab_off[si][k];  // computed ahead on the side stream
+              CU(cudaStreamWaitEvent(sh.stream, tab_ev[si][k], 0));
+            } else if (jit_table_cols(hb, &vl)) {
               const size_t need = (size_t)h.n_chunks * vl.width;
               if (need > sh.vtab_cap) {
                 if (sh.vtab) CU(cudaFree(sh.vtab));
@@ -780,8 +832,9 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
               }
               CU(launch_shape_table(dblob, sh.vtab, h.rank_base, h.n_chunks, vl, sh.stream));
               ctx->launches++;
+              vtab = sh.vtab;
             }
-            CU(jit_launch(fn, (int)grid, smem, dblob, hb, buf, h.rank_base, sh.vtab, xp, hb + h.off_pool,
+            CU(jit_launch(fn, (int)grid, smem, dblob, hb, buf, h.rank_base, vtab, xp, hb + h.off_pool,
                           pb, sh.stream));
             ctx->jit_launches++;
             ctx->jit_variant[jp.variant]++;
@@ -1003,6 +1056,7 @@ void qs_destroy(qs_ctx* ctx) {
     if (s.t0) cudaEventDestroy(s.t0);
     if (s.t1) cudaEventDestroy(s.t1);
     if (s.own_stream && s.stream) cudaStreamDestroy(s.stream);
+    if (s.side) cudaStreamDestroy(s.side);
   }
   if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
   if (ctx->host_tmp) cudaFreeHost(ctx->host_tmp);

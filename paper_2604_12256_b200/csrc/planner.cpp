@@ -14,6 +14,7 @@
 //   Virtual qubit map  logical -> physical; uncontrolled SWAPs are relabels
 //                      (Eq. 4).
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -699,7 +700,12 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
         u64 nn = need | tp;
         if (popc(nn) > kChunkBits) { defer(); continue; }
         const double c = (g.controls.empty() ? op_cost_unc(g.mat, g.is_h) : op_cost(g.mat, g.is_h)) + 0.5;
-        if (cost + c > budget && dense_taken > 0) { stop = true; defer(); continue; }
+        if (cost + c > budget && dense_taken > 0) {
+          if (budget == S.wo_budget) plan.stats.wo_budget_hit = true;
+          stop = true;
+          defer();
+          continue;
+        }
         // register layouts (assign_phases' greedy, on positions): a new
         // layout costs a shared-memory exchange; keep <= kMaxPhases/2
         {
@@ -1004,23 +1010,22 @@ int make_plan(const PlanInput& in, const std::vector<IrGate>& gates_in, Plan& pl
     if (rc == QS_OK) mark_pull_splits(plan, in.cfg);
     return rc;
   }
-  int rc = make_plan_budget(in, gates_in, plan, err, 40.0);
-  if (rc) return rc;
-  if (!in.product_state || plan.stats.n_passes < 3) {
-    mark_pull_splits(plan, in.cfg);
-    return QS_OK;
-  }
   // (more than 2 ranks: 40/48 only -- QAOA-32 on 4 GPUs takes 13 passes at
   // 64 but two of its fused-swap passes then run at half the NVLink rate:
   // 160.6 vs 135.7 ms with push/pull, measured per launch; on 2 GPUs the
   // 64-plan wins, 111.8 vs 116.2 ms.  QFT-32 on 4 GPUs needs 48 for 2 passes)
-  for (double b : {48.0, 64.0}) {
-    if (in.n_global > 1 && b > 48.0) break;
-    Plan alt;
-    std::string err2;
-    if (make_plan_budget(in, gates_in, alt, err2, b) == QS_OK && alt.stats.n_passes < plan.stats.n_passes)
-      plan = std::move(alt);
-  }
+  // Alternatives are planned only when the budget actually closed the
+  // write-only pass (otherwise they would produce the same plan).
+  int rc = make_plan_budget(in, gates_in, plan, err, 40.0);
+  if (rc) return rc;
+  if (in.product_state && plan.stats.n_passes >= 3 && plan.stats.wo_budget_hit)
+    for (double b : {48.0, 64.0}) {
+      if (in.n_global > 1 && b > 48.0) break;
+      Plan alt;
+      std::string err2;
+      if (make_plan_budget(in, gates_in, alt, err2, b) == QS_OK && alt.stats.n_passes < plan.stats.n_passes)
+        plan = std::move(alt);
+    }
   mark_pull_splits(plan, in.cfg);
   return QS_OK;
 }
@@ -1056,7 +1061,12 @@ static int make_plan_budget(const PlanInput& in, const std::vector<IrGate>& gate
   uint64_t full_gates = 0;
   for (const IrGate& g : gates) full_gates += g.n_src;
   plan.stats.paper_updates = before + (full_gates << in.n);
+  static const bool tdump = getenv("QS_PLAN_TIMING") != nullptr;  // diagnostics
+  auto ts = std::chrono::steady_clock::now();
   int rc = schedule(S, 0, in.n, plan.nl, map, std::move(gates), err);
+  if (tdump)
+    fprintf(stderr, "qs_plan schedule(full) %.3f ms\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ts).count());
   if (rc) return rc;
   if (S.src_mode) flush_source(S);  // circuit left nothing to fuse the source into
   plan.map_out = map;

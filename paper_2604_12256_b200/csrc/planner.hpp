@@ -100,6 +100,7 @@ struct PlanStats {
            n_fused_diag = 0, paper_updates = 0, naive_updates = 0,
            bytes_hbm = 0, bytes_nvlink = 0, n_fusable_swaps = 0;
   std::vector<std::vector<int>> booster_rounds;  // gate counts per round/group
+  bool wo_budget_hit = false;   // the FP64 budget closed the write-only pass
 };
 
 struct Plan {
