@@ -42,7 +42,7 @@ def test_random_sweep(qs, i):
         if rep == 1:   # a wide unitary and a QAOA / supremacy tail
             tg = tuple(int(q) for q in rng.permutation(n)[:5])
             gates.append(W.Gate("UNITARY", tg, (), (), W.haar_unitary(32, rng)))
-            gates += W.qaoa_maxcut(n, 1, seed)[n:]
+            gates += W.qaoa_maxcut(n, 1, seed, degree=3 if n % 2 == 0 else 4)[n:]
         if rep == 2:
             gates += W.supremacy_n(n, 4, seed)
         x = int(rng.integers(1 << n))
