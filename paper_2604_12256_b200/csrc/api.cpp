@@ -454,7 +454,13 @@ int execute(qs_ctx* ctx, const Plan& plan) {
   return rc;
 }
 
+static double ms_since(std::chrono::steady_clock::time_point t) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
+}
+
 int execute_steps(qs_ctx* ctx, const Plan& plan) {
+  static const bool tdump = getenv("QS_PLAN_TIMING") != nullptr;  // diagnostics
+  const auto te0 = std::chrono::steady_clock::now();
   ctx->n_fused_swaps = 0;  // per call (qs_stats_t reports the last call)
   ctx->fused_pending = false;
   // sub-state pool
@@ -524,6 +530,7 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
       o += (blobs[si].size() + 255) & ~(size_t)255;
     }
   }
+  if (tdump) fprintf(stderr, "qs_exec encode+upload %.3f ms\n", ms_since(te0));
   // Specialised kernels for every pass are compiled (in parallel) and loaded
   // before anything launches, so a failure cannot leave a half-applied plan:
   // a pass whose kernel is not ready runs on the interpreter kernel, and a
@@ -592,6 +599,7 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
   };
   std::vector<char> pulling(plan.steps.size(), 0);  // pull pass whose source was split
   ctx->prep_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count();
+  if (tdump) fprintf(stderr, "qs_exec prep %.3f ms\n", ctx->prep_ms);
   for (Shard& sh : ctx->shards) {
     CU(cudaSetDevice(sh.device));
     sh.timed.clear();
@@ -862,6 +870,7 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
       if (rc) return rc;
     }
   }
+  if (tdump) fprintf(stderr, "qs_exec launched %.3f ms after execute()\n", ms_since(te0));
   for (Shard& sh : ctx->shards) {
     CU(cudaSetDevice(sh.device));
     CU(cudaEventRecord(sh.t1, sh.stream));
@@ -899,6 +908,7 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
   }
   ctx->stats.t_swap_ms = tswap;
   ctx->stats.n_fused_swaps = ctx->n_fused_swaps;
+  if (tdump) fprintf(stderr, "qs_exec done %.3f ms after execute() (device %.3f ms)\n", ms_since(te0), tdev);
   return QS_OK;
 }
 
@@ -1108,10 +1118,16 @@ int qs_apply_circuit(qs_ctx* ctx, const qs_gate_t* gates, size_t n_gates) {
   in.product_state = ctx->pending;
   in.basis = ctx->basis;
   in.map = ctx->map;
+  auto tin = std::chrono::steady_clock::now();
   Plan plan;
   rc = make_plan(in, ir, plan, err);
   if (rc) return set_err(ctx, rc, err);
   auto t1 = std::chrono::steady_clock::now();
+  static const bool tdump = getenv("QS_PLAN_TIMING") != nullptr;  // diagnostics
+  if (tdump)
+    fprintf(stderr, "qs_apply ingest %.3f ms, plan %.3f ms\n",
+            std::chrono::duration<double, std::milli>(tin - t0).count(),
+            std::chrono::duration<double, std::milli>(t1 - tin).count());
   ctx->launches = 0;
   rc = execute(ctx, plan);
   if (rc) return rc;
