@@ -241,7 +241,11 @@ uint64_t qs_last_launches(const qs_ctx *ctx);
 
 /* Per-kernel device timing of the last qs_apply_circuit (CUDA events
  * recorded around every launch on the launching stream of the first local
- * shard).  Enabled by default; qs_set_timing(ctx, 0) disables it. */
+ * shard).  Enabled by default; qs_set_timing(ctx, 0) disables it;
+ * qs_set_timing(ctx, 2) makes the per-kernel timings, qs_last_launches and
+ * the t_plan_ms / t_device_ms statistics ADD UP over the following calls
+ * (a benchmark reads them once after its timed loop).  Every call of
+ * qs_set_timing resets them. */
 enum qs_kernel_id {
   QS_K1_CHUNK = 0,  /* multi-layout chunk kernel                          */
   QS_K2_DENSE = 1,  /* single-layout dense (fused matvec) pass            */

@@ -304,6 +304,10 @@ class Simulator:
     def launches(self) -> int:
         return int(self.lib.qs_last_launches(self.h))
 
+    def set_timing(self, mode: int):
+        """0 off, 1 per call (default), 2 accumulate over calls (qs_set_timing)."""
+        self._check(self.lib.qs_set_timing(self.h, int(mode)))
+
     def close(self):
         if self.h and self.h.value:
             self.lib.qs_destroy(self.h)

@@ -132,6 +132,8 @@ struct qs_ctx {
   double* host_tmp = nullptr;           // pinned readout staging
   size_t host_tmp_cap = 0;
   bool timing = true;
+  bool accumulate = false;  // qs_set_timing(ctx, 2): timings/launches/plan and device
+                            // times add up over calls until the next qs_set_timing
   uint64_t jit_launches = 0, jit_errors = 0;
   uint64_t jit_variant[JV_NUM] = {0, 0, 0, 0};  // launches per refill engine (handle lifetime)
   double prep_ms = 0;                           // last call: kernel preparation (compile/load)
@@ -887,10 +889,14 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
     CU(cudaEventElapsedTime(&ms, sh.t0, sh.t1));
     if (ms > tdev) tdev = ms;
   }
-  ctx->stats.t_device_ms = tdev;
-  memset(ctx->k_count, 0, sizeof ctx->k_count);
-  memset(ctx->k_ms, 0, sizeof ctx->k_ms);
-  memset(ctx->k_bytes, 0, sizeof ctx->k_bytes);
+  if (ctx->accumulate) {
+    ctx->stats.t_device_ms += tdev;
+  } else {
+    ctx->stats.t_device_ms = tdev;
+    memset(ctx->k_count, 0, sizeof ctx->k_count);
+    memset(ctx->k_ms, 0, sizeof ctx->k_ms);
+    memset(ctx->k_bytes, 0, sizeof ctx->k_bytes);
+  }
   double tswap = 0;
   if (ctx->timing) {
     Shard& s0 = ctx->shards[0];
@@ -1128,7 +1134,7 @@ int qs_apply_circuit(qs_ctx* ctx, const qs_gate_t* gates, size_t n_gates) {
     fprintf(stderr, "qs_apply ingest %.3f ms, plan %.3f ms\n",
             std::chrono::duration<double, std::milli>(tin - t0).count(),
             std::chrono::duration<double, std::milli>(t1 - tin).count());
-  ctx->launches = 0;
+  if (!ctx->accumulate) ctx->launches = 0;
   rc = execute(ctx, plan);
   if (rc) return rc;
   ctx->map = plan.map_out;
@@ -1149,7 +1155,8 @@ int qs_apply_circuit(qs_ctx* ctx, const qs_gate_t* gates, size_t n_gates) {
   s.bytes_nvlink = ps.bytes_nvlink;
   s.paper_updates = ps.paper_updates;
   s.naive_updates = ps.naive_updates;
-  s.t_plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  const double tp = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  s.t_plan_ms = ctx->accumulate ? s.t_plan_ms + tp : tp;
   return QS_OK;
 }
 
@@ -1334,6 +1341,13 @@ void* qs_get_stream(const qs_ctx* ctx, int i) {
 int qs_set_timing(qs_ctx* ctx, int enable) {
   if (!ctx) return QS_EINVAL;
   ctx->timing = enable != 0;
+  ctx->accumulate = enable == 2;
+  memset(ctx->k_count, 0, sizeof ctx->k_count);
+  memset(ctx->k_ms, 0, sizeof ctx->k_ms);
+  memset(ctx->k_bytes, 0, sizeof ctx->k_bytes);
+  ctx->stats.t_device_ms = 0;
+  ctx->stats.t_plan_ms = 0;
+  ctx->launches = 0;
   return QS_OK;
 }
 
