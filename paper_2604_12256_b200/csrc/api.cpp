@@ -95,8 +95,6 @@ struct Shard {
   ncclComm_t comm = nullptr;
   unsigned char* arena = nullptr;    // pass descriptors (device)
   size_t arena_cap = 0;
-  unsigned char* arena_pre = nullptr;  // descriptors of the sub-state prefix
-  size_t arena_pre_cap = 0;
   double2* subpool = nullptr;        // booster sub-states (device)
   size_t subpool_cap = 0;            // amplitudes
   double2* tmp = nullptr;            // readout gather buffer
@@ -131,7 +129,6 @@ struct qs_ctx {
   uint64_t launches = 0;
   unsigned char* host_stage = nullptr;  // pinned staging for descriptors
   size_t host_stage_cap = 0;
-  size_t host_stage_pre = 0;            // bytes of it the prefix upload uses
   double* host_tmp = nullptr;           // pinned readout staging
   size_t host_tmp_cap = 0;
   bool timing = true;
@@ -475,21 +472,9 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
     sub_off[i + 1] = sub_total;
     sub_total += (size_t)1 << plan.subs[i].nq;
   }
-  // Pass descriptors are encoded and uploaded in two parts: the leading
-  // sub-state steps (booster: sub-state init, interpreter passes, merges)
-  // go first and are launched at once, so their device work overlaps the
-  // encoding of the full-state passes.
-  std::vector<std::vector<size_t>> blob_off(ctx->shards.size(), std::vector<size_t>(plan.steps.size(), (size_t)-1));
-  std::vector<std::vector<unsigned char>> blobs_pre(ctx->shards.size()), blobs(ctx->shards.size());
-  std::vector<char> is_pre(plan.steps.size(), 0);
-  size_t npre = 0;
-  while (npre < plan.steps.size()) {
-    const Step& st = plan.steps[npre];
-    const bool sub_pass = st.type == Step::PASS && st.pass.buf != 0 &&
-                          (st.pass.kernel == KK_SMALL || st.pass.nl < ctx->cfg.jit_min_qubits);
-    if (!(st.type == Step::SUB_INIT || st.type == Step::SUB_MERGE || sub_pass)) break;
-    is_pre[npre++] = 1;
-  }
+  // encode all pass descriptors per shard
+  std::vector<std::vector<size_t>> blob_off(ctx->shards.size());
+  std::vector<std::vector<unsigned char>> blobs(ctx->shards.size());
   for (size_t si = 0; si < ctx->shards.size(); si++) {
     Shard& sh = ctx->shards[si];
     CU(cudaSetDevice(sh.device));
@@ -498,14 +483,10 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
       CU(cudaMalloc(&sh.subpool, sub_total * sizeof(double2)));
       sh.subpool_cap = sub_total;
     }
-  }
-  auto encode_range = [&](size_t k0, size_t k1, std::vector<std::vector<unsigned char>>& B) -> int {
-    for (size_t si = 0; si < ctx->shards.size(); si++) {
-      Shard& sh = ctx->shards[si];
-      std::vector<unsigned char>& all = B[si];
-      for (size_t k = k0; k < k1; k++) {
-        const Step& st = plan.steps[k];
-        if (st.type != Step::PASS) continue;
+    std::vector<unsigned char>& all = blobs[si];
+    for (const Step& st : plan.steps) {
+      size_t off = (size_t)-1;
+      if (st.type == Step::PASS) {
         std::vector<unsigned char> b;
         std::string err;
         const int rank = (st.pass.buf == 0) ? sh.rank : 0;
@@ -523,56 +504,90 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
           memcpy(b.data(), &h, sizeof h);
         }
         while (all.size() % 256) all.push_back(0);
-        blob_off[si][k] = all.size();
+        off = all.size();
         all.insert(all.end(), b.begin(), b.end());
       }
+      blob_off[si].push_back(off);
     }
-    return QS_OK;
-  };
-  // upload one part into an arena of each shard (grown when needed; an arena
-  // is never reallocated while a launched kernel may still read it: the
-  // prefix uses its own)
-  auto upload = [&](std::vector<std::vector<unsigned char>>& B, bool pre) -> int {
-    size_t stage_total = 0;
-    for (auto& b : B) stage_total += (b.size() + 255) & ~(size_t)255;
-    if (stage_total == 0) return QS_OK;
-    int rc = ensure_host_stage(ctx, stage_total + (pre ? 0 : ctx->host_stage_pre));
-    if (rc) return rc;
-    size_t o = pre ? 0 : ctx->host_stage_pre;
+    if (all.size() > sh.arena_cap) {
+      if (sh.arena) cudaFree(sh.arena);
+      size_t cap = std::max(all.size() * 2, (size_t)1 << 20);
+      CU(cudaMalloc(&sh.arena, cap));
+      sh.arena_cap = cap;
+    }
+  }
+  size_t stage_total = 0;
+  for (auto& b : blobs) stage_total += (b.size() + 255) & ~(size_t)255;
+  int rc = ensure_host_stage(ctx, stage_total);
+  if (rc) return rc;
+  {
+    size_t o = 0;
     for (size_t si = 0; si < ctx->shards.size(); si++) {
       Shard& sh = ctx->shards[si];
-      if (B[si].empty()) continue;
-      unsigned char*& arena = pre ? sh.arena_pre : sh.arena;
-      size_t& cap = pre ? sh.arena_pre_cap : sh.arena_cap;
+      if (blobs[si].empty()) continue;
+      memcpy(ctx->host_stage + o, blobs[si].data(), blobs[si].size());
       CU(cudaSetDevice(sh.device));
-      if (B[si].size() > cap) {
-        if (arena) cudaFree(arena);
-        arena = nullptr;
-        cap = 0;
-        const size_t c2 = std::max(B[si].size() * 2, (size_t)1 << 20);
-        CU(cudaMalloc(&arena, c2));
-        cap = c2;
-      }
-      memcpy(ctx->host_stage + o, B[si].data(), B[si].size());
-      CU(cudaMemcpyAsync(arena, ctx->host_stage + o, B[si].size(), cudaMemcpyHostToDevice, sh.stream));
-      o += (B[si].size() + 255) & ~(size_t)255;
+      CU(cudaMemcpyAsync(sh.arena, ctx->host_stage + o, blobs[si].size(),
+                         cudaMemcpyHostToDevice, sh.stream));
+      o += (blobs[si].size() + 255) & ~(size_t)255;
     }
-    if (pre) ctx->host_stage_pre = o;
-    return QS_OK;
-  };
-  auto hblob = [&](size_t si, size_t k) -> const unsigned char* {
-    return (is_pre[k] ? blobs_pre[si].data() : blobs[si].data()) + blob_off[si][k];
-  };
-  auto dblob_of = [&](size_t si, size_t k) -> const unsigned char* {
-    return (is_pre[k] ? ctx->shards[si].arena_pre : ctx->shards[si].arena) + blob_off[si][k];
-  };
-  int rc = QS_OK;
+  }
+  if (tdump) fprintf(stderr, "qs_exec encode+upload %.3f ms\n", ms_since(te0));
+  // Specialised kernels for every pass are compiled (in parallel) and loaded
+  // before anything launches, so a failure cannot leave a half-applied plan:
+  // a pass whose kernel is not ready runs on the interpreter kernel, and a
+  // swap fused into such a pass runs unfused.
+  const auto tp0 = std::chrono::steady_clock::now();
   std::vector<std::vector<JitPrepared>> prep(ctx->shards.size(), std::vector<JitPrepared>(plan.steps.size()));
   std::vector<char> step_jit(plan.steps.size(), 1);  // ready on every shard
+  for (size_t si = 0; si < ctx->shards.size(); si++) {
+    Shard& sh = ctx->shards[si];
+    std::vector<const unsigned char*> list;
+    std::vector<size_t> at;
+    for (size_t k = 0; k < plan.steps.size(); k++) {
+      const Step& st = plan.steps[k];
+      if (st.type != Step::PASS || st.pass.kernel == KK_SMALL || st.pass.nl < ctx->cfg.jit_min_qubits) {
+        step_jit[k] = 0;
+        continue;
+      }
+      list.push_back(blobs[si].data() + blob_off[si][k]);
+      at.push_back(k);
+    }
+    if (list.empty()) continue;
+    CU(cudaSetDevice(sh.device));
+    std::vector<JitPrepared> res;
+    jit_prepare_all(list, sh.device, res, false);
+    for (size_t i = 0; i < at.size(); i++) {
+      if (!res[i].ok) {
+        ctx->jit_errors++;
+        ctx->jit_last_error = res[i].err;
+        step_jit[at[i]] = 0;
+      }
+      prep[si][at[i]] = std::move(res[i]);
+    }
+  }
+  // fused swaps (f1) need the specialised kernel of the exporting pass on
+  // every rank: in rank mode all ranks vote (min) so they agree
+  bool any_fusable = false;
+  for (size_t k = 0; k + 1 < plan.steps.size(); k++)
+    if (plan.steps[k].type == Step::PASS && plan.steps[k].pass.x_j && plan.steps[k + 1].type == Step::SWAP &&
+        plan.steps[k + 1].fusable)
+      any_fusable = true;
   bool fuse_vote = true;
-  std::vector<char> pulling(plan.steps.size(), 0);  // pull pass whose source was split
-  std::vector<std::vector<size_t>> tab_off(ctx->shards.size(), std::vector<size_t>(plan.steps.size(), (size_t)-1));
-  std::vector<std::vector<cudaEvent_t>> tab_ev(ctx->shards.size(), std::vector<cudaEvent_t>(plan.steps.size(), nullptr));
+  if (any_fusable && ctx->mode == M_RANK && ctx->n_ranks > 1) {
+    double v = 1.0;
+    for (size_t k = 0; k < plan.steps.size(); k++)
+      if (plan.steps[k].type == Step::PASS && (plan.steps[k].pass.x_j || plan.steps[k].pass.pull_j) && !step_jit[k])
+        v = 0.0;
+    Shard& sh = ctx->shards[0];
+    CU(cudaSetDevice(sh.device));
+    double* dv = reinterpret_cast<double*>(sh.bar) + 1;
+    CU(cudaMemcpyAsync(dv, &v, sizeof v, cudaMemcpyHostToDevice, sh.stream));
+    NC(ncclAllReduce(dv, dv, 1, ncclDouble, ncclMin, sh.comm, sh.stream));
+    CU(cudaMemcpyAsync(&v, dv, sizeof v, cudaMemcpyDeviceToHost, sh.stream));
+    CU(cudaStreamSynchronize(sh.stream));
+    fuse_vote = v == 1.0;
+  }
   auto will_fuse = [&](size_t k) {
     if (k + 1 >= plan.steps.size()) return false;
     const Step& st = plan.steps[k];
@@ -584,8 +599,63 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
     return st.type == Step::PASS && st.pass.x_j && nx.type == Step::SWAP && nx.fusable && fuse_vote &&
            step_jit[k] && split_ok && ensure_peers(ctx) == 1;
   };
+  std::vector<char> pulling(plan.steps.size(), 0);  // pull pass whose source was split
+  ctx->prep_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count();
+  if (tdump) fprintf(stderr, "qs_exec prep %.3f ms\n", ctx->prep_ms);
+  for (Shard& sh : ctx->shards) {
+    CU(cudaSetDevice(sh.device));
+    sh.timed.clear();
+    sh.ev_used = 0;
+    CU(cudaEventRecord(sh.t0, sh.stream));
+  }
+  // Per-chunk tables (qs_kshape_table) depend only on the descriptors: all
+  // of them are computed on a side stream right at the start, so they
+  // overlap the passes before theirs instead of sitting in front of them
+  // (<= 1 GiB of tables per shard; else each is computed before its pass).
+  std::vector<std::vector<size_t>> tab_off(ctx->shards.size(), std::vector<size_t>(plan.steps.size(), (size_t)-1));
+  std::vector<std::vector<cudaEvent_t>> tab_ev(ctx->shards.size(), std::vector<cudaEvent_t>(plan.steps.size(), nullptr));
+  for (size_t si = 0; si < ctx->shards.size(); si++) {
+    Shard& sh = ctx->shards[si];
+    size_t total = 0;
+    std::vector<TabCols> cols(plan.steps.size());
+    for (size_t k = 0; k < plan.steps.size(); k++) {
+      if (!prep[si][k].ok) continue;
+      const unsigned char* hb = blobs[si].data() + blob_off[si][k];
+      if (!jit_table_cols(hb, &cols[k])) continue;
+      KPass h;
+      memcpy(&h, hb, sizeof h);
+      tab_off[si][k] = total;
+      total += ((size_t)h.n_chunks * cols[k].width + 31) & ~(size_t)31;
+    }
+    if (total == 0) continue;
+    if (total * sizeof(u64) > ((size_t)1 << 30)) {  // too much: tables per pass
+      for (size_t k = 0; k < plan.steps.size(); k++) tab_off[si][k] = (size_t)-1;
+      continue;
+    }
+    CU(cudaSetDevice(sh.device));
+    if (!sh.side) CU(cudaStreamCreateWithFlags(&sh.side, cudaStreamNonBlocking));
+    if (total > sh.vtab_cap) {
+      if (sh.vtab) CU(cudaFree(sh.vtab));
+      sh.vtab = nullptr;
+      sh.vtab_cap = 0;
+      CU(cudaMalloc(&sh.vtab, total * sizeof(u64)));
+      sh.vtab_cap = total;
+    }
+    CU(cudaStreamWaitEvent(sh.side, sh.t0, 0));
+    for (size_t k = 0; k < plan.steps.size(); k++) {
+      if (tab_off[si][k] == (size_t)-1) continue;
+      const unsigned char* hb = blobs[si].data() + blob_off[si][k];
+      KPass h;
+      memcpy(&h, hb, sizeof h);
+      CU(launch_shape_table(sh.arena + blob_off[si][k], sh.vtab + tab_off[si][k], h.rank_base, h.n_chunks, cols[k],
+                            sh.side));
+      ctx->launches++;
+      tab_ev[si][k] = get_event(sh);
+      CU(cudaEventRecord(tab_ev[si][k], sh.side));
+    }
+  }
   const size_t shard_amps = (size_t)1 << ctx->nl;
-  auto run_step = [&](size_t k) -> int {
+  for (size_t k = 0; k < plan.steps.size(); k++) {
     const Step& st = plan.steps[k];
     if (st.type == Step::SWAP) {
       Shard& s0 = ctx->shards[0];
@@ -639,7 +709,7 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
         CU(cudaEventRecord(b, s0.stream));
         s0.timed.push_back({KK_SWAP, a, b, (uint64_t)((16ull << ctx->nl) - (16ull << (ctx->nl - st.j)))});
       }
-      return QS_OK;
+      continue;
     }
     // A pass that stores into its peers' receive buffers may only start
     // once every peer is done with all earlier steps (an unfused swap's
@@ -722,9 +792,9 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
         }
         case Step::PASS: {
           const PassPlan& p = st.pass;
-          const unsigned char* dblob = dblob_of(si, k);
+          const unsigned char* dblob = sh.arena + blob_off[si][k];
           KPass h;
-          memcpy(&h, hblob(si, k), sizeof h);
+          memcpy(&h, blobs[si].data() + blob_off[si][k], sizeof h);
           double2* buf = (p.buf == 0) ? sh.state : (sh.subpool + sub_off[p.buf]);
           // fused swap: this pass exports the next swap's pieces (decided the
           // same way on every shard and rank: plan, kernel readiness vote,
@@ -754,7 +824,7 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
             if (getenv("QS_JIT_WO_MINB") && per_sm != 2 && grid > 8) grid &= ~7ull;
             if (jp.grid_mult > 1 && grid > (u64)jp.grid_mult) grid -= grid % (u64)jp.grid_mult;
             if (grid > h.n_chunks) grid = h.n_chunks;
-            const unsigned char* hb = hblob(si, k);
+            const unsigned char* hb = blobs[si].data() + blob_off[si][k];
             const size_t pb = jit_param_bytes(hb);
             TabCols vl;
             u64* vtab = sh.vtab;
@@ -801,144 +871,6 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
       rc = shard_barrier(ctx);
       if (rc) return rc;
     }
-    return QS_OK;
-  };
-  // 1. the sub-state prefix: encode, upload, launch
-  rc = encode_range(0, npre, blobs_pre);
-  if (rc) return rc;
-  rc = upload(blobs_pre, true);
-  if (rc) return rc;
-  bool t0_done = false;
-  auto record_t0 = [&]() -> int {
-    for (Shard& sh : ctx->shards) {
-      CU(cudaSetDevice(sh.device));
-      sh.timed.clear();
-      sh.ev_used = 0;
-      CU(cudaEventRecord(sh.t0, sh.stream));
-    }
-    t0_done = true;
-    return QS_OK;
-  };
-  if (npre) {
-    rc = record_t0();
-    if (rc) return rc;
-    for (size_t k = 0; k < npre; k++) {
-      rc = run_step(k);
-      if (rc) return rc;
-    }
-  }
-  // 2. the full-state steps
-  rc = encode_range(npre, plan.steps.size(), blobs);
-  if (rc) return rc;
-  rc = upload(blobs, false);
-  if (rc) return rc;
-  ctx->host_stage_pre = 0;
-  if (tdump) fprintf(stderr, "qs_exec encode+upload %.3f ms\n", ms_since(te0));
-  // Specialised kernels for every pass are compiled (in parallel) and loaded
-  // before anything launches, so a failure cannot leave a half-applied plan:
-  // a pass whose kernel is not ready runs on the interpreter kernel, and a
-  // swap fused into such a pass runs unfused.
-  const auto tp0 = std::chrono::steady_clock::now();
-  for (size_t si = 0; si < ctx->shards.size(); si++) {
-    Shard& sh = ctx->shards[si];
-    std::vector<const unsigned char*> list;
-    std::vector<size_t> at;
-    for (size_t k = 0; k < plan.steps.size(); k++) {
-      const Step& st = plan.steps[k];
-      if (st.type != Step::PASS || st.pass.kernel == KK_SMALL || st.pass.nl < ctx->cfg.jit_min_qubits) {
-        step_jit[k] = 0;
-        continue;
-      }
-      list.push_back(hblob(si, k));
-      at.push_back(k);
-    }
-    if (list.empty()) continue;
-    CU(cudaSetDevice(sh.device));
-    std::vector<JitPrepared> res;
-    jit_prepare_all(list, sh.device, res, false);
-    for (size_t i = 0; i < at.size(); i++) {
-      if (!res[i].ok) {
-        ctx->jit_errors++;
-        ctx->jit_last_error = res[i].err;
-        step_jit[at[i]] = 0;
-      }
-      prep[si][at[i]] = std::move(res[i]);
-    }
-  }
-  // fused swaps (f1) need the specialised kernel of the exporting pass on
-  // every rank: in rank mode all ranks vote (min) so they agree
-  bool any_fusable = false;
-  for (size_t k = 0; k + 1 < plan.steps.size(); k++)
-    if (plan.steps[k].type == Step::PASS && plan.steps[k].pass.x_j && plan.steps[k + 1].type == Step::SWAP &&
-        plan.steps[k + 1].fusable)
-      any_fusable = true;
-  if (any_fusable && ctx->mode == M_RANK && ctx->n_ranks > 1) {
-    double v = 1.0;
-    for (size_t k = 0; k < plan.steps.size(); k++)
-      if (plan.steps[k].type == Step::PASS && (plan.steps[k].pass.x_j || plan.steps[k].pass.pull_j) && !step_jit[k])
-        v = 0.0;
-    Shard& sh = ctx->shards[0];
-    CU(cudaSetDevice(sh.device));
-    double* dv = reinterpret_cast<double*>(sh.bar) + 1;
-    CU(cudaMemcpyAsync(dv, &v, sizeof v, cudaMemcpyHostToDevice, sh.stream));
-    NC(ncclAllReduce(dv, dv, 1, ncclDouble, ncclMin, sh.comm, sh.stream));
-    CU(cudaMemcpyAsync(&v, dv, sizeof v, cudaMemcpyDeviceToHost, sh.stream));
-    CU(cudaStreamSynchronize(sh.stream));
-    fuse_vote = v == 1.0;
-  }
-  ctx->prep_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count();
-  if (tdump) fprintf(stderr, "qs_exec prep %.3f ms\n", ctx->prep_ms);
-  if (!t0_done) {
-    rc = record_t0();
-    if (rc) return rc;
-  }
-  // Per-chunk tables (qs_kshape_table) depend only on the descriptors: all
-  // of them are computed on a side stream right at the start, so they
-  // overlap the passes before theirs instead of sitting in front of them
-  // (<= 1 GiB of tables per shard; else each is computed before its pass).
-  for (size_t si = 0; si < ctx->shards.size(); si++) {
-    Shard& sh = ctx->shards[si];
-    size_t total = 0;
-    std::vector<TabCols> cols(plan.steps.size());
-    for (size_t k = 0; k < plan.steps.size(); k++) {
-      if (!prep[si][k].ok) continue;
-      const unsigned char* hb = hblob(si, k);
-      if (!jit_table_cols(hb, &cols[k])) continue;
-      KPass h;
-      memcpy(&h, hb, sizeof h);
-      tab_off[si][k] = total;
-      total += ((size_t)h.n_chunks * cols[k].width + 31) & ~(size_t)31;
-    }
-    if (total == 0) continue;
-    if (total * sizeof(u64) > ((size_t)1 << 30)) {  // too much: tables per pass
-      for (size_t k = 0; k < plan.steps.size(); k++) tab_off[si][k] = (size_t)-1;
-      continue;
-    }
-    CU(cudaSetDevice(sh.device));
-    if (!sh.side) CU(cudaStreamCreateWithFlags(&sh.side, cudaStreamNonBlocking));
-    if (total > sh.vtab_cap) {
-      if (sh.vtab) CU(cudaFree(sh.vtab));
-      sh.vtab = nullptr;
-      sh.vtab_cap = 0;
-      CU(cudaMalloc(&sh.vtab, total * sizeof(u64)));
-      sh.vtab_cap = total;
-    }
-    CU(cudaStreamWaitEvent(sh.side, sh.t0, 0));
-    for (size_t k = 0; k < plan.steps.size(); k++) {
-      if (tab_off[si][k] == (size_t)-1) continue;
-      const unsigned char* hb = hblob(si, k);
-      KPass h;
-      memcpy(&h, hb, sizeof h);
-      CU(launch_shape_table(dblob_of(si, k), sh.vtab + tab_off[si][k], h.rank_base, h.n_chunks, cols[k],
-                            sh.side));
-      ctx->launches++;
-      tab_ev[si][k] = get_event(sh);
-      CU(cudaEventRecord(tab_ev[si][k], sh.side));
-    }
-  }
-  for (size_t k = npre; k < plan.steps.size(); k++) {
-    rc = run_step(k);
-    if (rc) return rc;
   }
   if (tdump) fprintf(stderr, "qs_exec launched %.3f ms after execute()\n", ms_since(te0));
   for (Shard& sh : ctx->shards) {
@@ -1131,7 +1063,6 @@ void qs_destroy(qs_ctx* ctx) {
     cudaFree(s.state);
     cudaFree(s.scratch);
     cudaFree(s.arena);
-    cudaFree(s.arena_pre);
     cudaFree(s.subpool);
     cudaFree(s.tmp);
     cudaFree(s.dmap);
