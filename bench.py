@@ -373,7 +373,7 @@ def main():
     dev_ms = st_acc["t_device_ms"]
     kt = {}
     for k in ("K1_chunk", "K2_dense", "K3_diag", "small", "K5_expand", "K5_merge", "init", "K4_swap",
-              "substate", "fused_swap_pass", "pull_pass"):
+              "substate", "fused_swap_pass", "pull_pass", "l2_group"):
         kt[k] = sim.kernel_timing(k)
     sim.set_timing(1)
     clk = clocks.stop()

@@ -94,6 +94,20 @@ typedef struct {
                              per-pass NVRTC-specialised kernels; 0 = all,
                              > 40 = none.  Default 18 (env QS_JIT=0/1
                              overrides the default to none / all).          */
+  int32_t l2_block_qubits; /* two-level blocking ("accommodated in
+                             the higher-level memory", "within the
+                             cache capacity"): consecutive
+                             full-state passes whose chunk and output
+                             positions all lie below this many qubits run
+                             block by block over contiguous blocks of at
+                             most 2^this amplitudes, so every pass after
+                             the first reads them from L2 instead of
+                             HBM (the passes of a run share one
+                             cooperative launch, block-level dataflow
+                             between them).  0 = off;
+                             else 14..40.  Default 0 (measured slower on
+                             B200; env QS_L2_BLOCK
+                             overrides the default).                      */
 } qs_config_t;
 
 /* ----------------------------------------------------------------- stats */
@@ -260,9 +274,12 @@ enum qs_kernel_id {
   QS_K1_FUSED_SWAP = 10, /* full-state pass that also performs the following
                             swap's exchange by NVLink peer stores (f1):
                             its time covers the pass AND the transfer       */
-  QS_K1_PULL = 11        /* the pass after a split fused swap: it loads the
+  QS_K1_PULL = 11,       /* the pass after a split fused swap: it loads the
                             half the exporting pass left in place from the
                             source ranks' buffers (NVLink reads)            */
+  QS_K1_L2_GROUP = 12    /* a run of passes executed wave by wave over
+                            L2-sized blocks (two-level blocking, f2): one
+                            entry per run; bytes = the run's HBM bytes      */
 };
 int qs_set_timing(qs_ctx *ctx, int enable);
 /* The cudaStream_t (as void*) the handle launches local shard `i` on, so a

@@ -38,7 +38,7 @@ KINDS = {
 }
 KERNELS = {"K1_chunk": 0, "K2_dense": 1, "K3_diag": 2, "small": 3, "K5_expand": 4,
            "K5_merge": 5, "init": 6, "K4_swap": 7, "K6_read": 8, "substate": 9,
-           "fused_swap_pass": 10, "pull_pass": 11}
+           "fused_swap_pass": 10, "pull_pass": 11, "l2_group": 12}
 
 
 class QSError(RuntimeError):
@@ -59,7 +59,8 @@ class qs_gate_t(ctypes.Structure):
 class qs_config_t(ctypes.Structure):
     _fields_ = [("chunk_qubits", ctypes.c_int32), ("fuse_cap", ctypes.c_int32),
                 ("diag_cap", ctypes.c_int32), ("boost_div", ctypes.c_int32),
-                ("flags", ctypes.c_uint32), ("jit_min_qubits", ctypes.c_int32)]
+                ("flags", ctypes.c_uint32), ("jit_min_qubits", ctypes.c_int32),
+                ("l2_block_qubits", ctypes.c_int32)]
 
 
 class qs_stats_t(ctypes.Structure):
@@ -181,10 +182,15 @@ def default_config() -> qs_config_t:
 
 def make_config(flags: int = QS_OPT_ALL, fuse_cap: int = 4, diag_cap: int = 0,
                 boost_div: int = 2, chunk_qubits: int = 12,
-                jit_min_qubits: Optional[int] = None) -> qs_config_t:
+                jit_min_qubits: Optional[int] = None,
+                l2_block_qubits: Optional[int] = None) -> qs_config_t:
+    d = default_config()
     if jit_min_qubits is None:
-        jit_min_qubits = default_config().jit_min_qubits
-    return qs_config_t(chunk_qubits, fuse_cap, diag_cap, boost_div, flags, jit_min_qubits)
+        jit_min_qubits = d.jit_min_qubits
+    if l2_block_qubits is None:
+        l2_block_qubits = d.l2_block_qubits
+    return qs_config_t(chunk_qubits, fuse_cap, diag_cap, boost_div, flags, jit_min_qubits,
+                       l2_block_qubits)
 
 
 def plan_json(n_qubits: int, gates: Sequence, n_ranks: int = 1, config: Optional[qs_config_t] = None,

@@ -43,8 +43,15 @@ int jit_prepare_all(const std::vector<const unsigned char*>& blobs, int device,
                     std::vector<JitPrepared>& out, bool compile_only);
 cudaError_t jit_launch(void* fn, int grid, size_t smem, const unsigned char* dblob,
                        const unsigned char* hblob, double2* state, u64 rank_base, const u64* vtab,
-                       const u64* xpeer8, const void* pool_host, size_t pool_bytes, cudaStream_t st);
+                       const u64* xpeer8, const void* pool_host, size_t pool_bytes, cudaStream_t st,
+                       u64 clo, u64 cn);
 int jit_table_cols(const unsigned char* blob, TabCols* v);
+bool jit_prepare_run(const std::vector<const unsigned char*>& blobs, int sb, int device, JitPrepared& out,
+                     bool compile_only = false);
+cudaError_t jit_launch_run(const JitPrepared& jp, int grid, const std::vector<const unsigned char*>& dblobs,
+                           const std::vector<const unsigned char*>& hblobs, double2* state, u64 rank_base,
+                           const std::vector<const u64*>& vtabs, u64 n_chunks, unsigned* flags, unsigned nblk,
+                           const unsigned* split, unsigned lag, cudaStream_t st);
 cudaError_t launch_shape_table(const unsigned char* dblob, u64* tab, u64 rank_base, u64 n_chunks,
                                const TabCols& v, cudaStream_t st);
 size_t jit_param_bytes(const unsigned char* blob);
@@ -100,6 +107,8 @@ struct Shard {
   double2* tmp = nullptr;            // readout gather buffer
   size_t tmp_cap = 0;                // amplitudes
   int8_t* dmap = nullptr;            // logical->physical map (device)
+  unsigned* l2flags = nullptr;       // per-block counters of co-scheduled runs (f2)
+  size_t l2flags_cap = 0;            // bytes
   u64* vtab = nullptr;               // per-chunk shape sums of the running pass
   size_t vtab_cap = 0;               // entries
   cudaStream_t side = nullptr;       // per-chunk tables of all passes, computed
@@ -135,6 +144,7 @@ struct qs_ctx {
   bool accumulate = false;  // qs_set_timing(ctx, 2): timings/launches/plan and device
                             // times add up over calls until the next qs_set_timing
   uint64_t jit_launches = 0, jit_errors = 0;
+  uint64_t n_l2_groups = 0;               // runs executed wave by wave (f2)
   uint64_t jit_variant[JV_NUM] = {0, 0, 0, 0};  // launches per refill engine (handle lifetime)
   double prep_ms = 0;                           // last call: kernel preparation (compile/load)
   std::string jit_last_error;
@@ -599,6 +609,53 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
     return st.type == Step::PASS && st.pass.x_j && nx.type == Step::SWAP && nx.fusable && fuse_vote &&
            step_jit[k] && split_ok && ensure_peers(ctx) == 1;
   };
+  // Co-scheduled runs (two-level blocking, f2; planner mark_l2_groups): up
+  // to kMaxRun consecutive passes of an L2 group become one cooperative
+  // launch (jit_prepare_run).  run_end[a] = one past the last pass of the run
+  // starting at step a (0: none); every shard must have it, else the passes
+  // run one by one.
+  std::vector<size_t> run_end(plan.steps.size(), 0);
+  std::vector<int> run_sb(plan.steps.size(), 0);
+  std::vector<std::vector<JitPrepared>> run_prep(ctx->shards.size(), std::vector<JitPrepared>(plan.steps.size()));
+  if (ctx->cfg.l2_block_qubits > 0 && !getenv("QS_NO_L2RUN")) {
+    for (size_t a = 0; a < plan.steps.size();) {
+      const Step& st = plan.steps[a];
+      if (st.type != Step::PASS || st.pass.l2_grp < 0) {
+        a++;
+        continue;
+      }
+      size_t b = a;
+      while (b < plan.steps.size() && b - a < (size_t)kMaxRun && plan.steps[b].type == Step::PASS &&
+             plan.steps[b].pass.l2_grp == st.pass.l2_grp)
+        b++;
+      if (b - a >= 2) {
+        int wm = kChunkBits;
+        for (size_t q = a; q < b; q++) {
+          for (int c : plan.steps[q].pass.cpos) wm = std::max(wm, c + 1);
+          for (int c : plan.steps[q].pass.opos) wm = std::max(wm, c + 1);
+        }
+        bool ok = true;
+        for (size_t si = 0; ok && si < ctx->shards.size(); si++) {
+          std::vector<const unsigned char*> hbs;
+          for (size_t q = a; q < b; q++) {
+            if (!prep[si][q].ok) ok = false;
+            hbs.push_back(blobs[si].data() + blob_off[si][q]);
+          }
+          if (!ok) break;
+          CU(cudaSetDevice(ctx->shards[si].device));
+          if (!jit_prepare_run(hbs, wm - kChunkBits, ctx->shards[si].device, run_prep[si][a])) {
+            ok = false;
+            ctx->jit_last_error = "run: " + run_prep[si][a].err;
+          }
+        }
+        if (ok) {
+          run_end[a] = b;
+          run_sb[a] = wm - kChunkBits;
+        }
+      }
+      a = b;
+    }
+  }
   std::vector<char> pulling(plan.steps.size(), 0);  // pull pass whose source was split
   ctx->prep_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count();
   if (tdump) fprintf(stderr, "qs_exec prep %.3f ms\n", ctx->prep_ms);
@@ -715,6 +772,113 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
     // once every peer is done with all earlier steps (an unfused swap's
     // local copy or a permute may still read the buffer that is now the
     // peer's receive buffer).
+    // Two-level blocking: a co-scheduled run of passes in
+    // one cooperative launch (jit_prepare_run); its per-chunk tables were
+    // computed ahead on the side stream (else the passes run one by one).
+    if (st.type == Step::PASS && run_end[k]) {
+      const size_t k1 = run_end[k];
+      bool ok = true;
+      for (size_t si = 0; ok && si < ctx->shards.size(); si++)
+        for (size_t q = k; ok && q < k1; q++) {
+          TabCols vl;
+          if (tab_off[si][q] == (size_t)-1 && jit_table_cols(blobs[si].data() + blob_off[si][q], &vl)) ok = false;
+        }
+      if (ok) {
+        const int K = (int)(k1 - k);
+        for (size_t si = 0; si < ctx->shards.size(); si++) {
+          Shard& sh = ctx->shards[si];
+          CU(cudaSetDevice(sh.device));
+          cudaEvent_t a = nullptr, b = nullptr;
+          if (ctx->timing) {
+            a = get_event(sh);
+            b = get_event(sh);
+            CU(cudaEventRecord(a, sh.stream));
+          }
+          std::vector<const unsigned char*> dbs, hbs;
+          std::vector<const u64*> vts;
+          u64 n_chunks = 0;
+          for (size_t q = k; q < k1; q++) {
+            dbs.push_back(sh.arena + blob_off[si][q]);
+            hbs.push_back(blobs[si].data() + blob_off[si][q]);
+            KPass h;
+            memcpy(&h, hbs.back(), sizeof h);
+            n_chunks = h.n_chunks;
+            const u64* vt = sh.vtab;
+            if (tab_off[si][q] != (size_t)-1) {
+              vt = sh.vtab + tab_off[si][q];
+              CU(cudaStreamWaitEvent(sh.stream, tab_ev[si][q], 0));
+            }
+            vts.push_back(vt);
+          }
+          const JitPrepared& rp = run_prep[si][k];
+          const unsigned nblk = (unsigned)(n_chunks >> run_sb[k]);
+          const size_t fbytes = (size_t)K * nblk * sizeof(unsigned);
+          if (fbytes > sh.l2flags_cap) {
+            if (sh.l2flags) CU(cudaFree(sh.l2flags));
+            sh.l2flags = nullptr;
+            sh.l2flags_cap = 0;
+            CU(cudaMalloc(&sh.l2flags, fbytes));
+            sh.l2flags_cap = fbytes;
+          }
+          CU(cudaMemsetAsync(sh.l2flags, 0, fbytes, sh.stream));
+          // the CTAs are dealt to the members by weight (QS_L2_SPLIT:
+          // comma-separated weights; default equal), each share a multiple
+          // of the members' grid multiple where possible
+          const int grid = num_sms_of(sh.device) * rp.per_sm;
+          std::vector<double> w(K, 1.0);
+          if (const char* e = getenv("QS_L2_SPLIT")) {
+            const char* c = e;
+            for (int i = 0; i < K && *c; i++) {
+              w[i] = atof(c);
+              while (*c && *c != ',') c++;
+              if (*c == ',') c++;
+            }
+          }
+          double wsum = 0;
+          for (double x : w) wsum += x;
+          unsigned split[kMaxRun];
+          unsigned at = 0;
+          for (int i = 0; i < K; i++) {
+            unsigned n_i = (unsigned)(grid * w[i] / wsum);
+            if (rp.grid_mult > 1 && n_i > (unsigned)rp.grid_mult) n_i -= n_i % (unsigned)rp.grid_mult;
+            if (n_i < 1) n_i = 1;
+            if (i == K - 1 || at + n_i > (unsigned)grid - (unsigned)(K - 1 - i)) n_i = (unsigned)grid - at - (unsigned)(K - 1 - i);
+            at += n_i;
+            split[i] = at;
+          }
+          // the first pass may run this far (QS_L2_LAG MiB, default 24) ahead
+          // of the last one
+          static const double lag_mib = getenv("QS_L2_LAG") ? atof(getenv("QS_L2_LAG")) : 24.0;
+          const double blk_mib = (double)(16ull << (kChunkBits + run_sb[k])) / (1 << 20);
+          // The lag must exceed what the members have in flight together: a
+          // member's ring loads up to 3 chunks of its CTA sequence ahead
+          // (3 x its CTA count in chunk order) before it finishes a chunk,
+          // and each member's loads wait for the one before it; with less
+          // lag the first member's throttle and the prefetches wait for each
+          // other.  Per member: 4 rounds of its CTAs, rounded up to blocks,
+          // plus one block.
+          unsigned min_lag = 1;
+          for (int i = 0; i < K; i++) {
+            const unsigned nb_i = split[i] - (i ? split[i - 1] : 0u);
+            min_lag += ((4u * nb_i + (1u << run_sb[k]) - 1u) >> run_sb[k]) + 1u;
+          }
+          const unsigned lag = std::max(min_lag, (unsigned)std::max(1.0, lag_mib / blk_mib));
+          CU(jit_launch_run(rp, grid, dbs, hbs, sh.state, (u64)sh.rank << ctx->nl, vts, n_chunks, sh.l2flags, nblk,
+                            split, lag, sh.stream));
+          ctx->launches += 2;
+          ctx->jit_launches++;
+          ctx->jit_variant[rp.variant]++;
+          if (ctx->timing) {
+            CU(cudaEventRecord(b, sh.stream));
+            const PassPlan& p0 = plan.steps[k].pass;
+            sh.timed.push_back({KK_L2, a, b, (uint64_t)((p0.src_mode ? 16ull : 32ull) << ctx->nl)});
+          }
+        }
+        ctx->n_l2_groups++;
+        k = k1 - 1;
+        continue;
+      }
+    }
     const bool fuse = will_fuse(k);
     if (fuse) {
       rc = shard_barrier(ctx);
@@ -845,7 +1009,7 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
               vtab = sh.vtab;
             }
             CU(jit_launch(fn, (int)grid, smem, dblob, hb, buf, h.rank_base, vtab, xp, hb + h.off_pool,
-                          pb, sh.stream));
+                          pb, sh.stream, 0, h.n_chunks));
             ctx->jit_launches++;
             ctx->jit_variant[jp.variant]++;
           } else {
@@ -935,6 +1099,10 @@ void qs_default_config(qs_config_t* cfg) {
   cfg->boost_div = 2;
   cfg->flags = QS_OPT_ALL;
   cfg->jit_min_qubits = jit_default_min();
+  // two-level blocking (f2) is off by default: on QFT-30 the co-scheduled
+  // run measured 15.8 ms against 9.2 ms pass by pass
+  static const int l2b = getenv("QS_L2_BLOCK") ? atoi(getenv("QS_L2_BLOCK")) : 0;
+  cfg->l2_block_qubits = l2b;
 }
 
 static int create_common(qs_ctx* ctx) {
@@ -1067,6 +1235,7 @@ void qs_destroy(qs_ctx* ctx) {
     cudaFree(s.tmp);
     cudaFree(s.dmap);
     cudaFree(s.vtab);
+    cudaFree(s.l2flags);
     cudaFree(s.bar);
     for (cudaEvent_t e : s.ev_pool) cudaEventDestroy(e);
     if (s.t0) cudaEventDestroy(s.t0);
@@ -1088,6 +1257,8 @@ int qs_set_config(qs_ctx* ctx, const qs_config_t* cfg) {
   if (cfg->boost_div < 1 || cfg->boost_div > 64) return set_err(ctx, QS_EINVAL, "boost_div in [1,64]");
   if (cfg->flags & ~QS_OPT_ALL) return set_err(ctx, QS_EINVAL, "unknown flags");
   if (cfg->jit_min_qubits < 0) return set_err(ctx, QS_EINVAL, "jit_min_qubits >= 0");
+  if (cfg->l2_block_qubits != 0 && (cfg->l2_block_qubits < 14 || cfg->l2_block_qubits > 40))
+    return set_err(ctx, QS_EINVAL, "l2_block_qubits 0 or in [14,40]");
   ctx->cfg = *cfg;
   return QS_OK;
 }
@@ -1317,13 +1488,13 @@ int64_t qs_jit_info(const qs_ctx* ctx, char* buf, size_t cap) {
   snprintf(b, sizeof b,
            "{\"jit_launches\":%llu,\"jit_errors\":%llu,\"compile_ms\":%.1f,\"compiles\":%llu,"
            "\"disk_hits\":%llu,\"prep_ms\":%.2f,\"variants\":{\"write_only\":%llu,\"bulk_tma\":%llu,"
-           "\"tensor_tma\":%llu,\"cp_async\":%llu},\"last_error\":\"%s\"}",
+           "\"tensor_tma\":%llu,\"cp_async\":%llu},\"l2_groups\":%llu,\"last_error\":\"%s\"}",
            (unsigned long long)(ctx ? ctx->jit_launches : 0),
            (unsigned long long)(ctx ? ctx->jit_errors : 0), ms, (unsigned long long)nc,
            (unsigned long long)hits, ctx ? ctx->prep_ms : 0.0,
            (unsigned long long)(v ? v[JV_WRITE_ONLY] : 0), (unsigned long long)(v ? v[JV_BULK] : 0),
            (unsigned long long)(v ? v[JV_TENSOR] : 0), (unsigned long long)(v ? v[JV_CPASYNC] : 0),
-           last.c_str());
+           (unsigned long long)(ctx ? ctx->n_l2_groups : 0), last.c_str());
   std::string s = b;
   if (buf && cap) {
     size_t k = std::min(cap - 1, s.size());

@@ -403,6 +403,23 @@ struct Gen {
   bool bad_op = false;        // an op type the generator does not know
   int variant = 0;            // chunk refill engine (JitVariant)
   int grid_mult = 1;          // the grid must be a multiple of this (hoisted expand gathers)
+  // Member of a co-scheduled run (two-level blocking): the
+  // pass is emitted as a device function qs_body() (the run kernel deals its
+  // CTAs to the passes of the run); run_wait: every chunk load first waits
+  // until the previous pass has stored its whole 2^(12+run_sb)-amplitude
+  // block (qs_fin counter); run_signal: every chunk's store is counted on
+  // its block (qs_fout) for the next pass.
+  bool run_mode = false, run_wait = false, run_signal = false;
+  // run_throttle (first member): chunk processing waits until the last
+  // member is done with the block qs_lag blocks back, so the run's blocks
+  // stay within L2 instead of the first pass racing ahead
+  bool run_throttle = false;
+  int run_sb = 0;             // chunk-id bits inside one block of the run
+  std::string run_wait_of(const std::string& c) const {
+    return run_wait ? "qs_wait(qs_fin + ((" + c + ") >> " + std::to_string(run_sb) + "), " +
+                          std::to_string(1 << run_sb) + "u); "
+                    : "";
+  }
   // Chunk groups per CTA: multi-layout load passes (compute-heavy between
   // their load and their store) run two groups over three buffers so a load
   // is always in flight; the others run one group (two CTAs per SM, one
@@ -1233,18 +1250,45 @@ struct Gen {
     }
     nthreads = kThreads * NG;
     const size_t npool = (h.total_bytes - h.off_pool) / sizeof(double);
-    param_pool = npool > 0 && npool <= kMaxParamPool;
+    param_pool = npool > 0 && npool <= kMaxParamPool && !run_mode;
     if (param_pool) o << "struct QsPool { double v[" << npool << "]; };\n";
     // fused swap: destination base per value of the exported
     // top local bits (receive buffers of this rank or its peers, by value)
     o << "struct QsXPeer { u64 v[16]; };\n";
+    if (run_mode) {
+      // QS_RUN_SLEEP (ns between polls), QS_RUN_NOPFENCE, QS_RUN_PROF
+      // (per-CTA wait cycles, printed by the run kernel): A/B and diagnostics
+      static const int sleep_ns = getenv("QS_RUN_SLEEP") ? atoi(getenv("QS_RUN_SLEEP")) : 64;
+      static const bool pfence = getenv("QS_RUN_NOPFENCE") == nullptr;
+      static const bool prof = getenv("QS_RUN_PROF") != nullptr;
+      // (a wait that lasts ~10 s means a scheduling bug: trap -- the launch
+      // fails with an error instead of hanging the device)
+      o << "__device__ __forceinline__ void qs_wait(const u32* f, u32 need) {\n"
+        << "  const long long t0_ = clock64();\n"
+        << "  for (;;) {\n    u32 v;\n"
+           "    asm volatile(\"ld.acquire.gpu.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(f) : \"memory\");\n"
+           "    if (v >= need) break;\n"
+           "    if (clock64() - t0_ > 20000000000ll) __trap();\n"
+        << (sleep_ns > 0 ? "    __nanosleep(" + std::to_string(sleep_ns) + ");\n" : "") << "  }\n"
+        << (pfence ? "  asm volatile(\"fence.proxy.async.global;\" ::: \"memory\");\n" : "")
+        << (prof ? "  if ((threadIdx.x & 31u) == 0) atomicAdd(&::qs_wcyc, (unsigned long long)(clock64() - t0_));\n" : "")
+        << "}\n";
+    }
     // QS_JIT_WO_MINB: A/B knob for the resident-CTA target of one-group passes
     static const int wo_minb = getenv("QS_JIT_WO_MINB") ? atoi(getenv("QS_JIT_WO_MINB")) : 2;
-    o << "extern \"C\" __global__ void __launch_bounds__(" << nthreads << ", " << (NG == 1 && NB <= 1 ? wo_minb : 1)
-      << ")\n" << kname
-      << "(const unsigned char* __restrict__ blob, double2* __restrict__ state, u64 rank_base, "
-         "const u64* __restrict__ vtab, const QsXPeer xp, const __grid_constant__ QsTmap tensmap"
-      << (param_pool ? ", const QsPool P" : "") << ") {\n";
+    if (run_mode)
+      o << "__device__ __forceinline__ void qs_body(const unsigned char* __restrict__ blob, double2* __restrict__ state, "
+           "u64 rank_base, const u64* __restrict__ vtab, const QsXPeer& xp, const QsTmap& tensmap, const u64 clo, "
+           "const u64 cn, const u32 qs_bid, const u32 qs_nbid, const u32* qs_fin, u32* qs_fout, const u32* qs_back, "
+           "const u32 qs_lag) {\n"
+           "  (void)qs_fin; (void)qs_fout; (void)qs_back; (void)qs_lag;\n";
+    else
+      o << "extern \"C\" __global__ void __launch_bounds__(" << nthreads << ", " << (NG == 1 && NB <= 1 ? wo_minb : 1)
+        << ")\n" << kname
+        << "(const unsigned char* __restrict__ blob, double2* __restrict__ state, u64 rank_base, "
+           "const u64* __restrict__ vtab, const QsXPeer xp, const __grid_constant__ QsTmap tensmap, "
+           "const u64 clo, const u64 cn"
+        << (param_pool ? ", const QsPool P" : "") << ") {\n";
     o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n";
     const size_t buf_bytes = (size_t)NB * CH * 16;
     // shape sums; with the per-chunk table, two copies: the chunk's and the
@@ -1278,6 +1322,7 @@ struct Gen {
     // of 228 KB, less the per-CTA reservation), minus the 4 KB sincos table
     // unless no sincos is left inside the loop (second generation pass)
     const long smem_cap = ((NG == 1 && NB <= 1) ? 113 * 1024 : 227 * 1024) - (table_free ? 0 : 4096) -
+                          (run_mode ? 12 * 1024 : 0) -
                           (ck_smem ? 16l * n_ck_entries() : 0l) - (mat_smem ? 8l * n_mat_doubles() : 0l);
     max_hoist = (int)std::max<long>(0, (smem_cap - (long)hz_off) / (kThreads * 16));
     if (max_hoist > 24) max_hoist = 24;
@@ -1293,7 +1338,9 @@ struct Gen {
       if (xchg || (pipe && !use_tma)) o << "  const int st" << p << " = swz(" << tc_expr(p) << ");\n";
     }
     o << "  const u64 tpo = " << tphys_expr(nlay - 1, true) << ";\n";
-    const std::string N = u(h.n_chunks);
+    // chunks [clo, clo + cn) of the pass's h.n_chunks: all of them, or one
+    // wave of an L2-blocked pass group (executor)
+    const std::string N = "cn";
     auto chunk_of = [&](const std::string& k) { return "(blockIdx.x + (u64)(" + k + ") * gridDim.x)"; };
 
     if (pipe) {
@@ -1311,7 +1358,8 @@ struct Gen {
     if (use_tma) {
       o << "  const int tcl0 = " << tc_expr(0) << ";\n";
       o << "  for (u32 k = grp; k < " << NB << "u; k += " << NG << "u)\n"
-        << "    if (tid < 32 && " << chunk_of("k") << " < " << N << ") { issue(state, corder(" << chunk_of("k") << ")"
+        << "    if (tid < 32 && " << chunk_of("k") << " < " << N << ") { "
+        << run_wait_of("corder(clo + " + chunk_of("k") + ")") << "issue(state, corder(clo + " << chunk_of("k") << ")"
         << ", bufs + k * " << CH << ", mbar + k, tid, &tensmap); if (tid == 0) issued[k] = 1u; }\n";
     } else if (pipe) {
       std::string tpd = "(0ull";
@@ -1319,12 +1367,13 @@ struct Gen {
         tpd += " | ((u64)((tid >> " + std::to_string(i) + ") & 1u) << " + std::to_string((int)h.cpos[i]) + ")";
       o << "  const u64 tpd = " << tpd << ");\n  const int sd = swz((int)tid);\n";
       o << "  for (u32 k = grp; k < " << NB << "u; k += " << NG << "u)\n"
-        << "    if (" << chunk_of("k") << " < " << N << ") { issue_async(state, corder(" << chunk_of("k") << ")"
+        << "    if (" << chunk_of("k") << " < " << N << ") { "
+        << run_wait_of("corder(clo + " + chunk_of("k") + ")") << "issue_async(state, corder(clo + " << chunk_of("k") << ")"
         << ", bufs + k * " << CH << ", mbar + k, tpd, sd); if (tid == 0) issued[k] = 1u; }\n";
     }
     if (PF > 0)
       o << "  for (u32 k = " << NB << "u + grp; k < " << NB + PF << "u; k += " << NG << "u)\n"
-        << "    if (tid < 32 && " << chunk_of("k") << " < " << N << ") l2pf(state, corder(" << chunk_of("k") << "), tid);\n";
+        << "    if (tid < 32 && " << chunk_of("k") << " < " << N << ") l2pf(state, corder(clo + " << chunk_of("k") << "), tid);\n";
     // level 1, constant shapes: once
     // level 1: one warp per shape, lanes over its terms, shuffle reduction
     auto level1 = [&](const char* map, size_t n, bool use_cphys) {
@@ -1351,10 +1400,10 @@ struct Gen {
     const std::string NV = std::to_string(W);
     if (warp_tab)
       o << "  { const u64 c0 = " << chunk_of("grp") << ";\n    if (lane < " << NV << "u && c0 < " << N
-        << ") wbase[lane] = __ldg(vtab + corder(c0) * " << NV << "ull + lane);\n    __syncwarp(); }\n";
+        << ") wbase[lane] = __ldg(vtab + corder(clo + c0) * " << NV << "ull + lane);\n    __syncwarp(); }\n";
     else if (use_vtab)
       o << "  { const u64 c0 = " << chunk_of("grp") << ";\n    if (tid < " << NV << "u && c0 < " << N
-        << ") scoef[tmap[tid]] = __ldg(vtab + corder(c0) * " << NV << "ull + tid); }\n  __syncthreads();\n";
+        << ") scoef[tmap[tid]] = __ldg(vtab + corder(clo + c0) * " << NV << "ull + tid); }\n  __syncthreads();\n";
     if (xh_g >= 0) {
       const int g = xh_g;
       o << "  double2* const xh = reinterpret_cast<double2*>(smem_raw + " << xh_off << ");\n"
@@ -1362,7 +1411,7 @@ struct Gen {
         << "  if (xinv) {\n"
         << "    const double2* __restrict__ xsv = reinterpret_cast<const double2*>(*reinterpret_cast<const u64*>(blob + "
         << (size_t)((const unsigned char*)&h.expand.ptr[g] - (const unsigned char*)&h) << "));\n"
-        << "    const u64 chunk = corder(" << chunk_of("grp") << ");\n"
+        << "    const u64 chunk = corder(clo + " << chunk_of("grp") << ");\n"
         << "    const u64 xph = (" << cbexpr << ") | rank_base | tp0;\n";
       for (int r = 0; r < kNReg; r++)
         o << "    xh[" << r * kThreads << " + tid] = __ldg(xsv + (((xph | " << u(reg_phys(0, r, false)) << ") >> "
@@ -1374,13 +1423,17 @@ struct Gen {
     o << "  for (u32 k = grp;; k += " << NG << "u) {\n"
       << "    const u64 craw = " << chunk_of("k") << ";\n"
       << "    if (craw >= " << N << ") break;\n"
-      << "    const u64 chunk = corder(craw);\n";
+      << "    const u64 chunk = corder(clo + craw);\n";
+    if (run_throttle)
+      o << "    if ((chunk >> " << run_sb << ") >= qs_lag) {\n"
+        << "      if (tid == 0) qs_wait(qs_back + ((chunk >> " << run_sb << ") - qs_lag), " << (1 << run_sb) << "u);\n"
+        << "      gbar(1u + grp);\n    }\n";
     if (pipe) o << "    const u32 kb = k % " << NB << "u;\n    double2* const sch = bufs + kb * " << CH << ";\n";
     else if (xchg) o << "    double2* const sch = bufs + grp * " << CH << ";\n";
     const std::string nxt = chunk_of("k + " + std::to_string(NB));
     const std::string pfc = chunk_of("k + " + std::to_string(NB + PF));
     const std::string pf_issue =
-        PF > 0 ? "    if (tid < 32 && " + pfc + " < " + N + ") l2pf(state, corder(" + pfc + "), tid);\n" : "";
+        PF > 0 ? "    if (tid < 32 && " + pfc + " < " + N + ") l2pf(state, corder(clo + " + pfc + "), tid);\n" : "";
     const std::string count = "if (tid == 0) { __threadfence_block(); issued[kb] = k / " +
                               std::to_string(NB) + "u + 2u; }";
     // QS_JIT_CHECK (debug builds of the kernels; compute-sanitizer is not
@@ -1395,9 +1448,9 @@ struct Gen {
     const std::string refill = poison +
         (use_tma ? "    gbar(1u + grp);  // every thread is done reading the buffer\n"
                   "    if (tid < 32 && " + nxt + " < " + N +
-                  ") { fence_proxy_async(); issue(state, corder(" + nxt + "), sch, mbar + kb, tid, &tensmap); " + count + " }\n" + pf_issue
+                  ") { " + run_wait_of("corder(clo + " + nxt + ")") + "fence_proxy_async(); issue(state, corder(clo + " + nxt + "), sch, mbar + kb, tid, &tensmap); " + count + " }\n" + pf_issue
                 : "    gbar(1u + grp);  // every thread is done reading the buffer\n"
-                  "    if (" + nxt + " < " + N + ") { issue_async(state, corder(" + nxt + "), sch, mbar + kb, tpd, sd); " +
+                  "    if (" + nxt + " < " + N + ") { " + run_wait_of("corder(clo + " + nxt + ")") + "issue_async(state, corder(clo + " + nxt + "), sch, mbar + kb, tpd, sd); " +
                   count + " }\n" + pf_issue);
     o << "    const u64 cb = " << cbexpr << ";\n";
     o << "    const u64 cphys = cb | rank_base;\n    (void)cphys;\n";
@@ -1417,10 +1470,10 @@ struct Gen {
       if (row_async)
         // the next row goes straight into the other copy with cp.async (a
         // register load gets sunk by the compiler next to its use)
-        o << "      if (lane < " << NV << "u && nc < " << N << ") cp_async8(wnx + lane, vtab + corder(nc) * " << NV
+        o << "      if (lane < " << NV << "u && nc < " << N << ") cp_async8(wnx + lane, vtab + corder(clo + nc) * " << NV
           << "ull + lane);\n      cp_async_commit(); }\n";
       else
-        o << "      u64 nxv = 0ull;\n      if (lane < " << NV << "u && nc < " << N << ") nxv = __ldg(vtab + corder(nc) * "
+        o << "      u64 nxv = 0ull;\n      if (lane < " << NV << "u && nc < " << N << ") nxv = __ldg(vtab + corder(clo + nc) * "
           << NV << "ull + lane);\n      nxrow = nxv; }\n";
     } else if (use_vtab) {
       // one coalesced table row per chunk instead of the level-1 term loops,
@@ -1431,7 +1484,7 @@ struct Gen {
         << "    (void)cisv;\n"
         << "    u64 nxv = 0ull;\n"
         << "    { const u64 nc = " << chunk_of("k + " + std::to_string(NG)) << ";\n"
-        << "      if (tid < " << NV << "u && nc < " << N << ") nxv = __ldg(vtab + corder(nc) * " << NV << "ull + tid); }\n";
+        << "      if (tid < " << NV << "u && nc < " << N << ") nxv = __ldg(vtab + corder(clo + nc) * " << NV << "ull + tid); }\n";
     } else if (!vary.empty()) {
       o << "    gbar(1u + grp);\n";
       if (!vbig.empty()) level1("vmap", vbig.size(), true);
@@ -1647,6 +1700,12 @@ struct Gen {
     if (warp_tab && row_async) o << "    cp_async_wait_group0();\n    __syncwarp();\n";
     else if (warp_tab) o << "    if (lane < " << NV << "u) wnx[lane] = nxrow;\n    __syncwarp();\n";
     else if (use_vtab) o << "    if (tid < " << NV << "u) scnx[tmap[tid]] = nxv;\n    gbar(1u + grp);\n";
+    if (run_signal)
+      // the group's stores of this chunk, then one release increment of its
+      // block's counter (cumulative over the barrier: the next pass's
+      // acquire sees all of them)
+      o << "    gbar(1u + grp);\n    if (tid == 0) asm volatile(\"red.release.gpu.global.add.u32 [%0], 1;\" :: \"l\"(qs_fout + (chunk >> "
+        << run_sb << ")) : \"memory\");\n";
     o << "  }\n";
     // peer stores must be performed before the barrier that publishes them
     if (h.x_mask) o << "  __threadfence_system();\n";
@@ -1714,6 +1773,8 @@ typedef CUresult (*PFN_ModuleLoadData)(CUmodule*, const void*);
 typedef CUresult (*PFN_ModuleGetFunction)(CUfunction*, CUmodule, const char*);
 typedef CUresult (*PFN_LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned,
                                      unsigned, unsigned, CUstream, void**, void**);
+typedef CUresult (*PFN_LaunchCoop)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                                   unsigned, CUstream, void**);
 typedef CUresult (*PFN_FuncSetAttribute)(CUfunction, CUfunction_attribute, int);
 typedef CUresult (*PFN_OccupancyMax)(int*, CUfunction, int, size_t);
 typedef CUresult (*PFN_TensorMapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -1729,6 +1790,7 @@ struct Driver {
   PFN_FuncSetAttribute setattr = nullptr;
   PFN_OccupancyMax occ = nullptr;
   PFN_TensorMapEncodeTiled tmap = nullptr;
+  PFN_LaunchCoop launch_coop = nullptr;
 };
 
 Driver& driver() {
@@ -1745,6 +1807,7 @@ Driver& driver() {
            get("cuFuncSetAttribute", (void**)&d.setattr) &&
            get("cuOccupancyMaxActiveBlocksPerMultiprocessor", (void**)&d.occ);
     if (d.ok && !get("cuTensorMapEncodeTiled", (void**)&d.tmap)) d.tmap = nullptr;
+    if (d.ok && !get("cuLaunchCooperativeKernel", (void**)&d.launch_coop)) d.launch_coop = nullptr;
   });
   return d;
 }
@@ -1829,13 +1892,28 @@ struct Source {
   bool ok = false;
 };
 
-Source make_source(const unsigned char* blob) {
+// run membership of a pass's generated code (f2; see Gen::run_mode)
+struct RunOpt {
+  bool wait = false, signal = false, throttle = false;
+  int sb = 0;
+};
+
+Source make_source(const unsigned char* blob, const RunOpt* ro = nullptr) {
   Source r;
   KPass h;
   memcpy(&h, blob, sizeof h);
   const char* kname = jit_kernel_name(h.kernel);
   const bool multi = h.kernel == KK_CHUNK, diag_only = h.kernel == KK_DIAG;
+  auto set_run = [&](Gen& x) {
+    if (!ro) return;
+    x.run_mode = true;
+    x.run_wait = ro->wait;
+    x.run_signal = ro->signal;
+    x.run_throttle = ro->throttle;
+    x.run_sb = ro->sb;
+  };
   Gen g(h, blob);
+  set_run(g);
   r.src = g.build(kname, multi, diag_only);
   r.smem = g.hz_off + (size_t)g.n_hoist * kThreads * 16;
   r.threads = g.nthreads;
@@ -1846,6 +1924,7 @@ Source make_source(const unsigned char* blob) {
   // every loop-invariant sincos out of the loop, no table is needed at all
   if (g.hoist_capped) {
     Gen g2(h, blob);
+    set_run(g2);
     g2.table_free = true;
     std::string s2 = g2.build(kname, multi, diag_only);
     if (g2.n_table == 0) {
@@ -2153,7 +2232,8 @@ bool jit_tensor_map(const unsigned char* blob, const void* state, void* out128) 
 
 cudaError_t jit_launch(void* fn, int grid, size_t smem, const unsigned char* dblob,
                        const unsigned char* hblob, double2* state, u64 rank_base, const u64* vtab,
-                       const u64* xpeer8, const void* pool_host, size_t pool_bytes, cudaStream_t st) {
+                       const u64* xpeer8, const void* pool_host, size_t pool_bytes, cudaStream_t st,
+                       u64 clo, u64 cn) {
   alignas(64) unsigned char tm[128];
   jit_tensor_map(hblob, state, tm);
   Driver& d = driver();
@@ -2167,10 +2247,222 @@ cudaError_t jit_launch(void* fn, int grid, size_t smem, const unsigned char* dbl
   memset(xp, 0, sizeof xp);
   if (xpeer8) memcpy(xp, xpeer8, sizeof xp);
   void* args[] = {(void*)&dblob, (void*)&state, (void*)&rank_base, (void*)&vtab, (void*)xp,
-                  (void*)tm, (void*)pool_host};
-  if (!pool_bytes) args[6] = nullptr;
+                  (void*)tm, (void*)&clo, (void*)&cn, (void*)pool_host};
+  if (!pool_bytes) args[8] = nullptr;
   CUresult r = d.launch((CUfunction)fn, (unsigned)grid, 1, 1, (unsigned)threads, 1, 1, (unsigned)smem,
                         (CUstream)st, args, nullptr);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorLaunchFailure;
+}
+
+// ------------------------------------------- co-scheduled runs (f2)
+// Two-level blocking (planner
+// mark_l2_groups): the K passes of a run execute in ONE cooperative launch.
+// Its CTAs are dealt to the passes (contiguous ranges, split.e[i] = first CTA
+// after member i); each member runs its own specialised chunk loop (the
+// generated pass code as qs_body in namespace qs_rI) over all chunks.  Member
+// i > 0 loads a chunk only after member i - 1 has stored every chunk of the
+// chunk's 2^(12 + sb)-amplitude block (per-block counters in `flags`, one
+// row of nblk per link): the blocks stream through the passes in order a
+// few MiB apart, so every member after the first reads them from L2 and the
+// state crosses HBM once.  Dependencies only point to lower members and all
+// CTAs are co-resident (cooperative launch), so the waits cannot deadlock.
+static const char* kRunKernel = "qs_run_jit";
+
+static std::string replace_all(std::string s, const std::string& a, const std::string& b) {
+  for (size_t p = s.find(a); p != std::string::npos; p = s.find(a, p + b.size())) s.replace(p, a.size(), b);
+  return s;
+}
+
+bool jit_prepare_run(const std::vector<const unsigned char*>& blobs, int sb, int device, JitPrepared& out,
+                     bool compile_only) {
+  out = JitPrepared();
+  const int K = (int)blobs.size();
+  if (K < 2 || K > kMaxRun) {
+    out.err = "run length";
+    return false;
+  }
+  std::vector<Source> m(K);
+  for (int i = 0; i < K; i++) {
+    RunOpt ro;
+    ro.wait = i > 0;
+    ro.signal = true;  // the last member's counters throttle the first
+    ro.throttle = i == 0;
+    ro.sb = sb;
+    m[i] = make_source(blobs[i], &ro);
+    if (!m[i].ok) {
+      out.err = m[i].err;
+      return false;
+    }
+    if (m[i].threads != m[0].threads) {
+      out.err = "run members differ in threads per CTA";
+      return false;
+    }
+  }
+  std::ostringstream o;
+  size_t smem = 0;
+  int gm = 1;
+  static const bool prof = getenv("QS_RUN_PROF") != nullptr;
+  o << "__shared__ unsigned long long qs_wcyc;\n";
+  for (int i = 0; i < K; i++) {
+    o << "namespace qs_r" << i << " {\n"
+      << replace_all(replace_all(m[i].src, "blockIdx.x", "qs_bid"), "gridDim.x", "qs_nbid") << "}\n";
+    smem = std::max(smem, m[i].smem);
+    gm = std::max(gm, m[i].grid_mult);
+  }
+  o << "struct __align__(64) QsTmapR { unsigned long long v[16]; };\n"
+    << "struct QsSplitR { unsigned int e[" << kMaxRun << "]; };\n"
+    << "extern \"C\" __global__ void __launch_bounds__(" << m[0].threads << ", 1)\n" << kRunKernel << "(";
+  for (int i = 0; i < K; i++) o << "const unsigned char* __restrict__ b" << i << ", ";
+  o << "double2* __restrict__ state, const unsigned long long rank_base, ";
+  for (int i = 0; i < K; i++) o << "const unsigned long long* __restrict__ v" << i << ", ";
+  for (int i = 0; i < K; i++) o << "const __grid_constant__ QsTmapR t" << i << ", ";
+  o << "const unsigned long long n_chunks, unsigned int* __restrict__ flags, const unsigned int nblk, "
+       "const QsSplitR split, const unsigned int lag) {\n"
+    << "  const unsigned int b = blockIdx.x;\n"
+    << (prof ? "  const long long qs_t0 = clock64();\n  if (threadIdx.x == 0) qs_wcyc = 0ull;\n  __syncthreads();\n" : "");
+  for (int i = 0; i < K; i++) {
+    const std::string lo = i ? "split.e[" + std::to_string(i - 1) + "]" : "0u";
+    o << "  " << (i ? "else if" : "if") << " (b < split.e[" << i << "]) {\n"
+      << "    const qs_r" << i << "::QsXPeer xz = {};\n"
+      << "    qs_r" << i << "::qs_body(b" << i << ", state, rank_base, v" << i << ", xz, reinterpret_cast<const qs_r" << i
+      << "::QsTmap&>(t" << i << "), 0ull, n_chunks, b - " << lo << ", split.e[" << i << "] - " << lo << ", "
+      << (i ? "flags + (size_t)" + std::to_string(i - 1) + " * nblk" : "nullptr") << ", "
+      << "flags + (size_t)" << i << " * nblk, flags + (size_t)" << K - 1 << " * nblk, lag);\n  }\n";
+  }
+  if (prof)
+    o << "  __syncthreads();\n"
+         "  if (threadIdx.x == 0 && (b % 8u) == 0u) {\n"
+         "    unsigned int r = 0; while (r < " << K - 1 << "u && b >= split.e[r]) r++;\n"
+         "    printf(\"qs_run_prof role %u cta %u cycles %lld wait_warp_cycles %llu\\n\", r, b, clock64() - qs_t0, qs_wcyc);\n  }\n";
+  o << "}\n";
+  const std::string src = o.str();
+  const u64 hash = fnv1a(src);
+  const u64 key = hash ^ ((u64)(device + 1) * 0x9E3779B97F4A7C15ull);
+  static std::unordered_map<u64, std::string> failed;  // a run kernel that did not build: not retried
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto f = failed.find(key);
+    if (f != failed.end()) {
+      out.err = f->second;
+      return false;
+    }
+    auto it = g_cache.find(key);
+    if (it != g_cache.end()) {
+      out.ok = true;
+      out.fn = (void*)it->second.f;
+      out.per_sm = it->second.blocks_per_sm;
+      out.smem = it->second.smem;
+      out.threads = it->second.threads;
+      out.grid_mult = it->second.grid_mult;
+      out.variant = it->second.variant;
+      return true;
+    }
+  }
+  char hx[32];
+  snprintf(hx, sizeof hx, "%016llx", (unsigned long long)hash);
+  const std::string dir = cache_dir();
+  const std::string path = dir + "/" + hx + ".cubin";
+  if (const char* dump = getenv("QS_JIT_DUMP"))
+    if (FILE* f = fopen((std::string(dump) + "/" + hx + "_" + kRunKernel + ".cu").c_str(), "wb")) {
+      fwrite(src.data(), 1, src.size(), f);
+      fclose(f);
+    }
+  std::vector<char> cubin;
+  if (read_file(path, cubin)) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_disk_hits++;
+  } else {
+    std::string err;
+    auto t0 = std::chrono::steady_clock::now();
+    if (!compile_cubin(src, kRunKernel, cubin, err)) {
+      out.err = err;
+      std::lock_guard<std::mutex> lk(g_mu);
+      failed[key] = err;
+      return false;
+    }
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    mkdir(dir.c_str(), 0755);
+    const std::string tmp = path + ".tmp" + std::to_string(getpid());
+    if (FILE* f = fopen(tmp.c_str(), "wb")) {
+      fwrite(cubin.data(), 1, cubin.size(), f);
+      fclose(f);
+      rename(tmp.c_str(), path.c_str());
+    }
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_compile_ms += ms;
+    g_compiles++;
+  }
+  if (compile_only) {
+    out.ok = true;
+    out.threads = m[0].threads;
+    out.smem = smem;
+    return true;
+  }
+  Driver& d = driver();
+  if (!d.ok || !d.launch_coop) {
+    out.err = "CUDA driver entry points unavailable";
+    return false;
+  }
+  CUmodule mod;
+  Compiled c;
+  if (d.load(&mod, cubin.data()) != CUDA_SUCCESS || d.getf(&c.f, mod, kRunKernel) != CUDA_SUCCESS) {
+    out.err = "run kernel: module load failed";
+    return false;
+  }
+  if (smem > 48 * 1024 && d.setattr(c.f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) != CUDA_SUCCESS) {
+    out.err = "run kernel: shared memory request refused";
+    return false;
+  }
+  int nb = 0;
+  if (d.occ(&nb, c.f, m[0].threads, smem) != CUDA_SUCCESS || nb < 1) {
+    out.err = "run kernel: does not fit on an SM";
+    return false;
+  }
+  c.blocks_per_sm = nb;
+  c.smem = smem;
+  c.threads = m[0].threads;
+  c.grid_mult = gm;
+  c.variant = m[K - 1].variant;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_cache[key] = c;
+    g_threads[(void*)c.f] = c.threads;
+  }
+  out.ok = true;
+  out.fn = (void*)c.f;
+  out.per_sm = nb;
+  out.smem = smem;
+  out.threads = c.threads;
+  out.grid_mult = gm;
+  out.variant = c.variant;
+  return true;
+}
+
+cudaError_t jit_launch_run(const JitPrepared& jp, int grid, const std::vector<const unsigned char*>& dblobs,
+                           const std::vector<const unsigned char*>& hblobs, double2* state, u64 rank_base,
+                           const std::vector<const u64*>& vtabs, u64 n_chunks, unsigned* flags, unsigned nblk,
+                           const unsigned* split, unsigned lag, cudaStream_t st) {
+  const int K = (int)dblobs.size();
+  alignas(64) unsigned char tm[kMaxRun][128];
+  std::vector<void*> args;
+  for (int i = 0; i < K; i++) args.push_back((void*)&dblobs[i]);
+  args.push_back((void*)&state);
+  args.push_back((void*)&rank_base);
+  for (int i = 0; i < K; i++) args.push_back((void*)&vtabs[i]);
+  for (int i = 0; i < K; i++) {
+    jit_tensor_map(hblobs[i], state, tm[i]);
+    args.push_back((void*)tm[i]);
+  }
+  unsigned sp[kMaxRun];
+  for (int i = 0; i < kMaxRun; i++) sp[i] = i < K ? split[i] : 0u;
+  args.push_back((void*)&n_chunks);
+  args.push_back((void*)&flags);
+  args.push_back((void*)&nblk);
+  args.push_back((void*)sp);
+  args.push_back((void*)&lag);
+  Driver& d = driver();
+  CUresult r = d.launch_coop((CUfunction)jp.fn, (unsigned)grid, 1, 1, (unsigned)jp.threads, 1, 1, (unsigned)jp.smem,
+                             (CUstream)st, args.data());
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorLaunchFailure;
 }
 

@@ -995,6 +995,7 @@ static int booster(Sched& S, int n, std::vector<IrGate>& gates, std::string& err
 static int make_plan_budget(const PlanInput& in, const std::vector<IrGate>& gates_in, Plan& plan,
                             std::string& err, double wo_budget);
 static void mark_pull_splits(Plan& plan, const qs_config_t& cfg);
+static void mark_l2_groups(Plan& plan, const qs_config_t& cfg);
 
 // The write-only first pass (booster / basis source fused) gets an FP64
 // budget (c15): about the work its 16 B/amp of writes hide (~40 FP64/amp).
@@ -1007,7 +1008,10 @@ int make_plan(const PlanInput& in, const std::vector<IrGate>& gates_in, Plan& pl
   const char* e = getenv("QS_WO_BUDGET");  // experiment knob
   if (e && *e) {
     const int rc = make_plan_budget(in, gates_in, plan, err, atof(e));
-    if (rc == QS_OK) mark_pull_splits(plan, in.cfg);
+    if (rc == QS_OK) {
+      mark_pull_splits(plan, in.cfg);
+      mark_l2_groups(plan, in.cfg);
+    }
     return rc;
   }
   // (more than 2 ranks: 40/48 only -- QAOA-32 on 4 GPUs takes 13 passes at
@@ -1027,6 +1031,7 @@ int make_plan(const PlanInput& in, const std::vector<IrGate>& gates_in, Plan& pl
         plan = std::move(alt);
     }
   mark_pull_splits(plan, in.cfg);
+  mark_l2_groups(plan, in.cfg);
   return QS_OK;
 }
 
@@ -1113,6 +1118,51 @@ static void mark_pull_splits(Plan& plan, const qs_config_t& cfg) {
     pn.pull_z = z;
     pn.pull_pos = sw.lpos;
   }
+}
+
+// Two-level blocking (the state of a gate block
+// is "accommodated in the higher-level memory ... and processed
+// consecutively"; C "within the cache capacity").  Level 1 is the
+// 2^12-amplitude chunk of one CTA (shared memory, Alg. 2).  Level 2 is a
+// contiguous block of 2^W amplitudes (W = cfg.l2_block_qubits): a pass whose
+// chunk and output positions all lie below W maps every such block onto
+// itself, so a run of consecutive such passes can be executed block by block
+// -- a wave of chunks [b 2^(W-12), (b+1) 2^(W-12)) through every pass of the
+// run before the next wave -- and every pass after a wave's first finds the
+// wave in L2.  The run's HBM traffic is one read (none for a write-only
+// first pass) and one write of the state.  Fused-swap exporters and pull
+// passes talk to peers and stay outside.
+static void mark_l2_groups(Plan& plan, const qs_config_t& cfg) {
+  const int W = cfg.l2_block_qubits;
+  plan.stats.bytes_hbm_l2 = plan.stats.bytes_hbm;
+  if (W <= 0 || plan.nl <= W) return;
+  auto eligible = [&](const Step& st) {
+    if (st.type != Step::PASS) return false;
+    const PassPlan& p = st.pass;
+    if (p.buf != 0 || p.nl != plan.nl || p.kernel == KK_SMALL || p.nl < cfg.jit_min_qubits) return false;
+    if (p.x_j || p.x_split >= 0 || p.pull_j) return false;
+    for (int c : p.cpos)
+      if (c >= W) return false;
+    for (int c : p.opos)
+      if (c >= W) return false;
+    return true;
+  };
+  int g = 0;
+  for (size_t i = 0; i < plan.steps.size();) {
+    size_t j = i;
+    while (j < plan.steps.size() && eligible(plan.steps[j])) j++;
+    if (j - i >= 2) {
+      for (size_t k = i; k < j; k++) {
+        plan.steps[k].pass.l2_grp = g;
+        // every pass after the first: L2 only (algorithmic HBM bytes)
+        if (k > i) plan.stats.bytes_hbm_l2 -= (uint64_t)32 << plan.nl;
+      }
+      // the first pass's write reaches HBM only through the last one
+      g++;
+    }
+    i = j > i ? j : i + 1;
+  }
+  plan.stats.n_l2_groups = (uint64_t)g;
 }
 
 // ------------------------------------------------------------ encoding
@@ -1562,7 +1612,8 @@ std::string plan_to_json(const Plan& plan, bool detail) {
     << ",\"n_swaps\":" << s.n_swaps << ",\"n_fusable_swaps\":" << s.n_fusable_swaps << ",\"n_sub_gates\":" << s.n_sub_gates
     << ",\"n_fused_diag\":" << s.n_fused_diag << ",\"paper_updates\":" << s.paper_updates
     << ",\"naive_updates\":" << s.naive_updates << ",\"bytes_hbm\":" << s.bytes_hbm
-    << ",\"bytes_nvlink\":" << s.bytes_nvlink << ",\"booster_rounds\":[";
+    << ",\"bytes_nvlink\":" << s.bytes_nvlink << ",\"n_l2_groups\":" << s.n_l2_groups
+    << ",\"bytes_hbm_l2\":" << s.bytes_hbm_l2 << ",\"booster_rounds\":[";
   for (size_t r = 0; r < s.booster_rounds.size(); r++) {
     o << (r ? "," : "") << "[";
     for (size_t g = 0; g < s.booster_rounds[r].size(); g++)
@@ -1614,7 +1665,7 @@ std::string plan_to_json(const Plan& plan, bool detail) {
         const PassPlan& p = st.pass;
         o << "\"type\":\"pass\",\"kernel\":\"" << kname(p.kernel) << "\",\"buf\":" << p.buf
           << ",\"nl\":" << p.nl << ",\"src_mode\":" << p.src_mode << ",\"x_j\":" << p.x_j
-          << ",\"x_split\":" << p.x_split << ",\"pull_j\":" << p.pull_j << ",\"pull_z\":" << p.pull_z
+          << ",\"x_split\":" << p.x_split << ",\"pull_j\":" << p.pull_j << ",\"pull_z\":" << p.pull_z << ",\"l2_grp\":" << p.l2_grp
           << ",\"x_pos\":[" << (p.x_j > 0 ? std::to_string(p.x_pos[0]) : "")
           << (p.x_j > 1 ? "," + std::to_string(p.x_pos[1]) : "") << (p.x_j > 2 ? "," + std::to_string(p.x_pos[2]) : "")
           << "]"

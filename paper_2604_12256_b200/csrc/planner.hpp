@@ -69,6 +69,9 @@ struct PassPlan {
   int x_split = -1;
   int pull_j = 0, pull_z = -1;
   std::vector<int> pull_pos;
+  // two-level blocking: id of the run of consecutive passes
+  // executed wave by wave over L2-sized blocks (-1: none)
+  int l2_grp = -1;
   // filled by encode_pass
   std::vector<std::vector<int>> phase_regs;  // per phase: chunk bits held in registers
   std::vector<int> op_phase;
@@ -98,7 +101,8 @@ struct PlanStats {
   uint64_t n_gates_in = 0, n_passes = 0, n_chunk = 0, n_dense = 0, n_diag = 0,
            n_small = 0, n_expand = 0, n_swaps = 0, n_sub_gates = 0,
            n_fused_diag = 0, paper_updates = 0, naive_updates = 0,
-           bytes_hbm = 0, bytes_nvlink = 0, n_fusable_swaps = 0;
+           bytes_hbm = 0, bytes_nvlink = 0, n_fusable_swaps = 0,
+           n_l2_groups = 0, bytes_hbm_l2 = 0;  // f2: runs, HBM bytes with them
   std::vector<std::vector<int>> booster_rounds;  // gate counts per round/group
   bool wo_budget_hit = false;   // the FP64 budget closed the write-only pass
 };

@@ -24,6 +24,7 @@ constexpr int kMaxShapes = 1024;          // diag shapes per pass (smem)
 constexpr int kMaxRuns = 16;              // runs of the chunk-id deposit
 constexpr int kMaxExpand = 4;             // sub-states multiplied by K5
 constexpr int kMaxVaryTab = 64;           // chunk-dependent shapes read from a table
+constexpr int kMaxRun = 4;                 // passes per co-scheduled run (f2)
 constexpr int kMaxXBits = 3;              // fused-swap export bits (2^3 destinations)
 
 // Kernel kinds (stats / timing ids).
@@ -42,7 +43,9 @@ enum KernelKind {
                   // exchange by NVLink peer stores (f1; timing class only)
   KK_PULL = 11,   // full-state pass that loads the other half of a split
                   // swap from the source ranks' buffers (timing class only)
-  KK_NUM = 12
+  KK_L2 = 12,     // a run of passes executed wave by wave over L2-sized
+                  // blocks (f2; timing class only)
+  KK_NUM = 13
 };
 
 // Register-op types inside a pass.

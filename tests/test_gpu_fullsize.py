@@ -222,3 +222,30 @@ def test_unit_scaled_ops_and_pass_scales(qs, jit):
     psi = s.state()
     s.close()
     check(psi, n, circ, basis=5)
+
+
+@pytest.mark.parametrize("wbits", [15, 18, 21])
+def test_l2_blocked_runs_n24(qs, wbits):
+    """Two-level blocking: runs of passes whose positions
+    lie below W execute wave by wave over 2^W-amplitude blocks (2^(24-W)
+    waves, each launch covering a chunk range).  QFT-24 from a basis state
+    (both passes grouped) and a random circuit whose dense gates act below W
+    (every pass grouped), against the oracle."""
+    n = 24
+    low = ([W.Gate("H", (q,)) for q in range(n)] +
+           W.random_circuit(wbits, 200, 2411 + wbits, diag_bias=0.4, max_generic=2) +
+           W.random_circuit(n, 40, 7, diag_bias=0.9))   # dense work below W, phases anywhere
+    cases = [(W.qft(n), 0x9E3779 % (1 << n)), (low, 12345)]
+    for gates, basis in cases:
+        cfg = qs.make_config(l2_block_qubits=wbits)
+        plan = qs.plan_json(n, gates, config=cfg, basis=basis)
+        assert plan["stats"]["n_l2_groups"] >= 1
+        s = qs.Simulator(n)
+        s.set_config(cfg)
+        s.set_basis_state(basis)
+        s.apply(gates)
+        psi = s.state()
+        info = qs.jit_info(s)
+        s.close()
+        assert info["jit_errors"] == 0 and info["l2_groups"] >= 1
+        check(psi, n, gates, basis=basis)

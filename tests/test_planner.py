@@ -366,3 +366,30 @@ def test_unit_scaled_gates_replay(name):
     gates += W.random_circuit(n, 40, 3)
     _, psi = run(n, gates, basis=9)
     assert np.max(np.abs(psi - oracle.apply_circuit(n, gates, x=9))) < 1e-11
+
+
+def test_l2_groups_marked_by_position_bound():
+    """Two-level blocking: runs of >= 2
+    consecutive full-state passes whose chunk and output positions all lie
+    below W are marked as one group; off (0) by default; the HBM bytes of a
+    group are its first pass's."""
+    n = 26
+    gates = W.qft(n)
+    assert qs.plan_json(n, gates)["stats"]["n_l2_groups"] == 0
+    for wb in (15, 18, 22):
+        p = qs.plan_json(n, gates, config=qs.make_config(l2_block_qubits=wb), basis=5)
+        full = [s for s in p["steps"] if s["type"] == "pass" and s["nl"] == n]
+        grouped = [s for s in full if s["l2_grp"] >= 0]
+        assert p["stats"]["n_l2_groups"] >= 1 and len(grouped) >= 2
+        for s in grouped:
+            assert max(s["cpos"] + s["opos"]) < wb
+            assert s["x_j"] == 0 and s["pull_j"] == 0
+        saved = 0
+        for g in set(s["l2_grp"] for s in grouped):
+            saved += (sum(1 for s in grouped if s["l2_grp"] == g) - 1) * (32 << n)
+        assert p["stats"]["bytes_hbm_l2"] == p["stats"]["bytes_hbm"] - saved
+    # a bound below the passes' positions: nothing grouped
+    p = qs.plan_json(n, gates, config=qs.make_config(l2_block_qubits=14), basis=5)
+    assert all(max(s["cpos"] + s["opos"]) < 14 for s in p["steps"]
+               if s["type"] == "pass" and s.get("l2_grp", -1) >= 0)
+
