@@ -155,6 +155,9 @@ struct qs_ctx {
   int peers = 0;
   std::vector<double2*> ipc;
   bool fused_pending = false;
+  // the last circuit's launches are enqueued but not yet waited for
+  // (accumulating timing mode: finish_inflight)
+  bool inflight = false;
   uint64_t n_fused_swaps = 0;
   // per kernel kind: launches, ms, algorithmic bytes (last call, shard 0..)
   uint64_t k_count[KK_NUM];
@@ -457,6 +460,7 @@ int exec_swap(qs_ctx* ctx, const Step& st) {
 
 // -------------------------------------------------------------- execute
 int execute_steps(qs_ctx* ctx, const Plan& plan);
+int finish_inflight(qs_ctx* ctx);
 
 // Every error after the first launch leaves a partly applied circuit:
 // the handle is poisoned (include/qs.h, qs_apply_circuit).
@@ -473,8 +477,6 @@ static double ms_since(std::chrono::steady_clock::time_point t) {
 int execute_steps(qs_ctx* ctx, const Plan& plan) {
   static const bool tdump = getenv("QS_PLAN_TIMING") != nullptr;  // diagnostics
   const auto te0 = std::chrono::steady_clock::now();
-  ctx->n_fused_swaps = 0;  // per call (qs_stats_t reports the last call)
-  ctx->fused_pending = false;
   // sub-state pool
   std::vector<size_t> sub_off(plan.subs.size() + 1, 0);
   size_t sub_total = 0;
@@ -526,6 +528,15 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
       sh.arena_cap = cap;
     }
   }
+  // the previous circuit (accumulating mode: still in flight) must be done
+  // before its staging buffer, descriptors and events are reused; the
+  // planning and encoding above overlapped it
+  {
+    const int rc = finish_inflight(ctx);
+    if (rc) return rc;
+  }
+  ctx->n_fused_swaps = 0;  // per call (qs_stats_t reports the last call)
+  ctx->fused_pending = false;
   size_t stage_total = 0;
   for (auto& b : blobs) stage_total += (b.size() + 255) & ~(size_t)255;
   int rc = ensure_host_stage(ctx, stage_total);
@@ -1041,6 +1052,21 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
     CU(cudaSetDevice(sh.device));
     CU(cudaEventRecord(sh.t1, sh.stream));
   }
+  ctx->inflight = true;
+  // In the accumulating timing mode (qs_set_timing 2, a loop of circuits)
+  // the call returns once everything is enqueued: the next call's planning
+  // and encoding overlap this circuit's device work, and the completion is
+  // taken at the next call or at any query (finish_inflight).
+  if (ctx->accumulate) return QS_OK;
+  return finish_inflight(ctx);
+}
+
+// Wait for the enqueued circuit, then account its device time and per-kernel
+// timings (execute_steps).  A device error found here poisons the handle.
+int finish_inflight(qs_ctx* ctx) {
+  if (!ctx->inflight) return QS_OK;
+  ctx->inflight = false;
+  static const bool tdump = getenv("QS_PLAN_TIMING") != nullptr;  // diagnostics
   for (Shard& sh : ctx->shards) {
     CU(cudaSetDevice(sh.device));
     CU(cudaStreamSynchronize(sh.stream));
@@ -1078,7 +1104,7 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
   }
   ctx->stats.t_swap_ms = tswap;
   ctx->stats.n_fused_swaps = ctx->n_fused_swaps;
-  if (tdump) fprintf(stderr, "qs_exec done %.3f ms after execute() (device %.3f ms)\n", ms_since(te0), tdev);
+  if (tdump) fprintf(stderr, "qs_exec done (device %.3f ms)\n", tdev);
   return QS_OK;
 }
 
@@ -1393,15 +1419,27 @@ static int readout(qs_ctx* ctx, double* host_out, uint64_t offset, uint64_t coun
 }
 
 int qs_get_state(qs_ctx* ctx, double* host_out, uint64_t offset, uint64_t count) {
+  if (ctx) {
+    const int rc = finish_inflight(ctx);
+    if (rc) return rc;
+  }
   return readout(ctx, host_out, offset, count, 0);
 }
 
 int qs_probabilities(qs_ctx* ctx, double* host_out, uint64_t offset, uint64_t count) {
+  if (ctx) {
+    const int rc = finish_inflight(ctx);
+    if (rc) return rc;
+  }
   return readout(ctx, host_out, offset, count, 1);
 }
 
 int qs_get_stats(const qs_ctx* ctx, qs_stats_t* out) {
   if (!ctx || !out) return QS_EINVAL;
+  {
+    const int rc = finish_inflight(const_cast<qs_ctx*>(ctx));
+    if (rc) return rc;
+  }
   *out = ctx->stats;
   return QS_OK;
 }
@@ -1511,6 +1549,10 @@ void* qs_get_stream(const qs_ctx* ctx, int i) {
 
 int qs_set_timing(qs_ctx* ctx, int enable) {
   if (!ctx) return QS_EINVAL;
+  {
+    const int rc = finish_inflight(ctx);
+    if (rc) return rc;
+  }
   ctx->timing = enable != 0;
   ctx->accumulate = enable == 2;
   memset(ctx->k_count, 0, sizeof ctx->k_count);
@@ -1525,6 +1567,10 @@ int qs_set_timing(qs_ctx* ctx, int enable) {
 int qs_get_kernel_timing(const qs_ctx* ctx, int kind, uint64_t* launches, double* ms,
                          uint64_t* bytes) {
   if (!ctx || kind < 0 || kind >= KK_NUM) return QS_EINVAL;
+  {
+    const int rc = finish_inflight(const_cast<qs_ctx*>(ctx));
+    if (rc) return rc;
+  }
   if (launches) *launches = ctx->k_count[kind];
   if (ms) *ms = ctx->k_ms[kind];
   if (bytes) *bytes = ctx->k_bytes[kind];

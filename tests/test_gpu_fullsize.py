@@ -249,3 +249,32 @@ def test_l2_blocked_runs_n24(qs, wbits):
         s.close()
         assert info["jit_errors"] == 0 and info["l2_groups"] >= 1
         check(psi, n, gates, basis=basis)
+
+
+def test_accumulating_mode_back_to_back_circuits(qs):
+    """qs_set_timing(2): a call returns once its launches are enqueued and the
+    next call's planning overlaps them; results, device time and per-kernel
+    counts are taken at the next call or query.  Three back-to-back QFT-22
+    circuits from different basis states: the last state matches the oracle
+    and the accumulated launch counts are three times one call's."""
+    n = 22
+    gates = W.qft(n)
+    s = qs.Simulator(n)
+    s.set_basis_state(1)
+    s.apply(gates)
+    s.set_timing(1)
+    s.set_basis_state(2)
+    s.apply(gates)
+    one = {k: s.kernel_timing(k)["launches"] for k in ("K1_chunk", "K2_dense", "K3_diag")}
+    s.set_timing(2)
+    for x in (0x15, 0x2A5, 0x3FF0F):
+        s.set_basis_state(x)
+        s.apply(gates)
+    acc = {k: s.kernel_timing(k)["launches"] for k in ("K1_chunk", "K2_dense", "K3_diag")}
+    st = s.stats()
+    psi = s.state()
+    s.set_timing(0)
+    s.close()
+    assert acc == {k: 3 * v for k, v in one.items()}
+    assert st["t_device_ms"] > 0
+    check(psi, n, gates, basis=0x3FF0F)
