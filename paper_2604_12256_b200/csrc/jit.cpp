@@ -1236,17 +1236,60 @@ struct Gen {
     // shared-memory ring): cp.async.bulk.prefetch.L2 of chunk k + NB + PF
     // when chunk k's buffer is refilled, so DRAM latency overlaps more than
     // the one chunk load the ring keeps in flight.  QS_JIT_L2PF: A/B knob.
+    // Per engine: tensor passes prefetch with the same tensor copies
+    // (cp.async.bulk.prefetch.tensor), bulk passes per contiguous run
+    // (>= 512 B), per-thread cp.async passes one prefetch.global.L2 per
+    // 128 B line (the threads holding a line's first element); round 1's
+    // bulk prefetch of every 64-256 B run lost badly (QAOA-30 90 -> 151 ms).
     static const int l2pf = getenv("QS_JIT_L2PF") ? atoi(getenv("QS_JIT_L2PF")) : 0;
-    const int PF = pipe ? l2pf : 0;
-    if (PF > 0) {
-      o << "__device__ __forceinline__ void l2pf(const double2* __restrict__ state, u64 chunk, u32 lane) {\n"
-        << "  const u64 cb = " << cbexpr << ";\n"
+    const int PF = (pipe && !pull) ? l2pf : 0;
+    const bool pf_all = PF > 0 && !use_tma;  // every thread of the group prefetches
+    if (PF > 0 && use_tensor) {
+      const int ncopy = 1 << tp.n_extra;
+      o << "__device__ __forceinline__ void l2pf(const double2* __restrict__ state, u64 chunk, u32 lane, const QsTmap* tm) {\n"
+        << "  (void)state;\n  const u64 cb = " << cbexpr << ";\n"
+        << "  for (u32 e = lane; e < " << ncopy << "u; e += 32u) {\n"
+        << "    asm volatile(\"cp.async.bulk.prefetch.tensor." << tp.rank << "d.L2.global.tile [%0, {";
+      for (int d = 0; d < tp.rank; d++) o << (d ? ", " : "") << "%" << d + 1;
+      o << "}];\"\n      :: \"l\"(tm)";
+      for (int d = 0; d < tp.rank; d++) {
+        if (tp.chunk[d]) {
+          o << ", \"r\"(0)";
+        } else if (d == 4 && tp.n_extra) {
+          o << ", \"r\"((u32)((cb >> " << tp.pos[d] << ") & " << ((1ull << tp.len[d]) - 1) << "ull)";
+          for (int x = 0; x < tp.n_extra; x++)
+            o << " | (((e >> " << x << ") & 1u) << " << tp.extra[x] - tp.pos[4] << ")";
+          o << ")";
+        } else {
+          o << ", \"r\"((u32)((cb >> " << tp.pos[d] << ") & " << ((1ull << tp.len[d]) - 1) << "ull))";
+        }
+      }
+      o << " : \"memory\");\n  }\n}\n";
+    } else if (PF > 0 && use_tma) {
+      o << "__device__ __forceinline__ void l2pf(const double2* __restrict__ state, u64 chunk, u32 lane, const QsTmap* tm) {\n"
+        << "  (void)tm;\n  const u64 cb = " << cbexpr << ";\n"
         << "  for (int seg = (int)lane; seg < " << nseg << "; seg += 32) {\n"
         << "    const u64 off = 0ull";
       for (int i = 0; i < kChunkBits - l; i++)
         o << " | ((u64)((seg >> " << i << ") & 1) << " << (int)h.cpos[l + i] << ")";
       o << ";\n    asm volatile(\"cp.async.bulk.prefetch.L2.global [%0], %1;\" :: \"l\"(state + (cb | off)), \"r\"("
         << (16 << l) << "u) : \"memory\");\n  }\n}\n";
+    } else if (PF > 0) {
+      // thread t's elements t + 256 i: chunk bits 0..2 are positions 0..2
+      // (the forced low run), so threads t = 0 mod 8 start every line
+      o << "__device__ __forceinline__ void l2pf(const double2* __restrict__ state, u64 chunk, u32 tid, const QsTmap* tm) {\n"
+        << "  (void)tm;\n  if ((tid & 7u) != 0u) return;\n"
+        << "  const u64 cb = " << cbexpr << ";\n"
+        << "  const double2* sp = state + (cb";
+      for (int i = 0; i < kLogT; i++) o << " | ((u64)((tid >> " << i << ") & 1u) << " << (int)h.cpos[i] << ")";
+      o << ");\n";
+      for (int i = 0; i < kNReg; i++) {
+        u64 off = 0;
+        for (int k = 0; k < kRegBits; k++)
+          if (i >> k & 1) off |= 1ull << h.cpos[kLogT + k];
+        o << "  asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(sp + " << u(off) << ") : \"memory\");\n";
+      }
+      o << "}\n";
     }
     nthreads = kThreads * NG;
     const size_t npool = (h.total_bytes - h.off_pool) / sizeof(double);
@@ -1373,7 +1416,8 @@ struct Gen {
     }
     if (PF > 0)
       o << "  for (u32 k = " << NB << "u + grp; k < " << NB + PF << "u; k += " << NG << "u)\n"
-        << "    if (tid < 32 && " << chunk_of("k") << " < " << N << ") l2pf(state, corder(clo + " << chunk_of("k") << "), tid);\n";
+        << "    if (" << (pf_all ? "" : "tid < 32 && ") << chunk_of("k") << " < " << N << ") l2pf(state, corder(clo + "
+        << chunk_of("k") << "), tid, &tensmap);\n";
     // level 1, constant shapes: once
     // level 1: one warp per shape, lanes over its terms, shuffle reduction
     auto level1 = [&](const char* map, size_t n, bool use_cphys) {
@@ -1433,7 +1477,9 @@ struct Gen {
     const std::string nxt = chunk_of("k + " + std::to_string(NB));
     const std::string pfc = chunk_of("k + " + std::to_string(NB + PF));
     const std::string pf_issue =
-        PF > 0 ? "    if (tid < 32 && " + pfc + " < " + N + ") l2pf(state, corder(clo + " + pfc + "), tid);\n" : "";
+        PF > 0 ? "    if (" + std::string(pf_all ? "" : "tid < 32 && ") + pfc + " < " + N + ") l2pf(state, corder(clo + " + pfc +
+                     "), tid, &tensmap);\n"
+               : "";
     const std::string count = "if (tid == 0) { __threadfence_block(); issued[kb] = k / " +
                               std::to_string(NB) + "u + 2u; }";
     // QS_JIT_CHECK (debug builds of the kernels; compute-sanitizer is not
