@@ -628,7 +628,10 @@ int execute_steps(qs_ctx* ctx, const Plan& plan) {
   std::vector<size_t> run_end(plan.steps.size(), 0);
   std::vector<int> run_sb(plan.steps.size(), 0);
   std::vector<std::vector<JitPrepared>> run_prep(ctx->shards.size(), std::vector<JitPrepared>(plan.steps.size()));
-  if (ctx->cfg.l2_block_qubits > 0 && !getenv("QS_NO_L2RUN")) {
+  // (loopback shards share one device: their cooperative launches would
+  // compete for the same SMs, so runs are used with one shard per device)
+  if (ctx->cfg.l2_block_qubits > 0 && !getenv("QS_NO_L2RUN") &&
+      (ctx->mode != M_LOOPBACK || ctx->shards.size() == 1)) {
     for (size_t a = 0; a < plan.steps.size();) {
       const Step& st = plan.steps[a];
       if (st.type != Step::PASS || st.pass.l2_grp < 0) {

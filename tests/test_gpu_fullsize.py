@@ -278,3 +278,20 @@ def test_accumulating_mode_back_to_back_circuits(qs):
     assert acc == {k: 3 * v for k, v in one.items()}
     assert st["t_device_ms"] > 0
     check(psi, n, gates, basis=0x3FF0F)
+
+
+def test_l2_runs_not_used_on_loopback_shards(qs):
+    """Loopback shards share one device, so marked runs execute pass by pass
+    there (two cooperative launches would compete for the same SMs)."""
+    n = 24
+    gates = W.qft(n)
+    cfg = qs.make_config(l2_block_qubits=18)
+    s = qs.Simulator(n, loopback_ranks=2)
+    s.set_config(cfg)
+    s.set_basis_state(77)
+    s.apply(gates)
+    psi = s.state()
+    info = qs.jit_info(s)
+    s.close()
+    assert info["l2_groups"] == 0
+    check(psi, n, gates, basis=77)
