@@ -292,7 +292,7 @@ def main():
     ap.add_argument("--qubits", "--n", dest="n", type=int, default=0,
                     help="override qubit count (--qubits under torchrun: its parser claims --n)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
