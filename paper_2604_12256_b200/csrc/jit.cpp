@@ -1384,7 +1384,23 @@ struct Gen {
     // chunks [clo, clo + cn) of the pass's h.n_chunks: all of them, or one
     // wave of an L2-blocked pass group (executor)
     const std::string N = "cn";
-    auto chunk_of = [&](const std::string& k) { return "(blockIdx.x + (u64)(" + k + ") * gridDim.x)"; };
+    // Chunk pairs: a two-group load pass deals chunk PAIRS
+    // (2m, 2m + 1; m = blockIdx.x + j gridDim.x) to its groups, so the loads
+    // a CTA has in flight differ in chunk-id bit 0 (the lowest non-chunk
+    // position) -- probe: a chunk without position 3 or 5 streams at 0.75 of
+    // the bandwidth of one with it (scripts/dev/pattern_bw.cu)
+    // Default: the passes whose chunk has neither position 3 nor 5 (the
+    // slow address pattern); QS_JIT_PAIR=0 never, =1 every two-group load pass.
+    static const int pair_env = getenv("QS_JIT_PAIR") ? atoi(getenv("QS_JIT_PAIR")) : -1;
+    bool slow_pattern = true;
+    for (int c = 0; c < kChunkBits; c++)
+      if (h.cpos[c] == 3 || h.cpos[c] == 5) slow_pattern = false;
+    const bool pair = (pair_env == 1 || (pair_env < 0 && slow_pattern)) && pipe && NG == 2 && xh_g < 0 &&
+                      (h.n_chunks % 2) == 0;
+    auto chunk_of = [&](const std::string& k) {
+      return pair ? "(((((u64)blockIdx.x + (u64)((" + k + ") >> 1) * gridDim.x)) << 1) | (u64)((" + k + ") & 1u))"
+                  : "(blockIdx.x + (u64)(" + k + ") * gridDim.x)";
+    };
 
     if (pipe) {
       o << "  if (threadIdx.x == 0) {\n"

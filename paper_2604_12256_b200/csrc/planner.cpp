@@ -566,8 +566,14 @@ static void finalize_chunk_pass(Sched& S, PassPlan& p, u64 need_pos, int nl,
     }
     std::stable_sort(cand.begin(), cand.end(), [](const Cand& a, const Cand& b) { return a.use < b.use; });
     // give output positions 0,1,2 to the 3 best lane-bit chunk bits; the
-    // chunk bits that fed them take the vacated positions
-    for (int slot = 0; slot < 3; slot++) {
+    // chunk bits that fed them take the vacated positions.  Position 3 too
+    // when this chunk has it: a chunk with position 3 (or 5) streams at full
+    // HBM bandwidth, one with neither at ~0.75-0.8 of it (address-pattern
+    // probe, scripts/dev/pattern_bw.cu), so the next pass should find a
+    // target there (QS_NO_STEER3: A/B knob)
+    static const bool steer3 = !getenv("QS_NO_STEER3");
+    const int nslot = (steer3 && nlane >= 4 && std::find(p.opos.begin(), p.opos.end(), 3) != p.opos.end()) ? 4 : 3;
+    for (int slot = 0; slot < nslot; slot++) {
       const int c = cand[slot].c;
       if (p.opos[c] == slot) continue;
       int holder = -1;
@@ -596,7 +602,9 @@ static int schedule(Sched& S, int buf, int nq, int nl, std::vector<int>& map,
   Plan& plan = *S.plan;
   const int n_global = nq - nl;
   const bool blocking = (S.cfg->flags & QS_OPT_BLOCK) != 0;
-  const int l = 3;  // low positions always in a chunk (128 B runs); 3,4 added when room
+  // low positions always in a chunk (128 B runs); 3,4 added when room.
+  // QS_PLAN_LOW: A/B knob for the forced low run
+  static const int l = getenv("QS_PLAN_LOW") ? atoi(getenv("QS_PLAN_LOW")) : 3;
   std::vector<IrGate> rem;
   // A fused diagonal with more distinct monomials than one pass can encode
   // (kMaxShapes) is split into commuting factors (phase polynomials add).
