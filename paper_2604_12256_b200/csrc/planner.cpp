@@ -584,6 +584,34 @@ static void finalize_chunk_pass(Sched& S, PassPlan& p, u64 need_pos, int nl,
       if (qa >= 0) mp[qa] = slot;
       if (qb >= 0) mp[qb] = p.opos[holder];
     }
+    // position 5 is the other fast-pattern position: any chunk bit may be
+    // stored there (coalescing needs only 0,1,2 on lane bits), so it could
+    // get the soonest-needed qubit of the rest of the chunk.  QS_STEER5=1
+    // (A/B knob, off: on the plans it trades QAOA-30's fast-pattern passes
+    // 7 -> 5 for rand-30's 19 -> 23, and rand's fast/slow gap is small)
+    static const bool steer5 = getenv("QS_STEER5") != nullptr && atoi(getenv("QS_STEER5")) != 0;
+    int h5 = -1;
+    for (size_t k = 0; k < p.opos.size(); k++)
+      if (p.opos[k] == 5) h5 = (int)k;
+    if (steer3 && steer5 && h5 >= 0) {
+      int best = -1;
+      long bu = (long)1 << 40;
+      for (size_t k = 0; k < p.opos.size(); k++) {
+        if (p.opos[k] < nslot) continue;  // placed on 0..3 above
+        const int q = qubit_at(p.opos[k]);
+        const long u = q >= 0 ? next_use(q) : ((long)1 << 41);
+        if (u < bu) {
+          bu = u;
+          best = (int)k;
+        }
+      }
+      if (best >= 0 && best != h5) {
+        const int qa = qubit_at(p.opos[best]), qb = qubit_at(5);
+        std::swap(p.opos[best], p.opos[h5]);
+        if (qa >= 0) mp[qa] = 5;
+        if (qb >= 0) mp[qb] = p.opos[h5];
+      }
+    }
   }
   if (S.src_mode && p.buf == 0) {
     p.src_mode = S.src_mode;
