@@ -214,6 +214,42 @@ static bool unit_scaled(const std::vector<cd>& m, cd* lam_out, std::vector<cd>* 
   return true;
 }
 
+// An uncontrolled one-qubit matrix [[a, b], [c, d]] is applied as
+// lam [[a, b], [c, d]] / lam with lam = the larger of a, b (|lam| >= 1/sqrt2
+// for a unitary, so every ratio has magnitude <= 1): entries equal to
+// +-lam, +-i lam become exact units (built from the comparison, like
+// unit_scaled) and lam joins the pass scale.  RX = cos [[1, -i tan],
+// [-i tan, 1]] then costs 2 FP64 per output amplitude instead of 4 (the
+// kernels bake units into additions, dense()), RY likewise.  false: no
+// entry became a unit (nothing to gain).  QS_NO_ROWSCALE: A/B knob.
+static bool row_scale_1q(std::vector<cd>& m, cd* lam_out) {
+  static const bool off = getenv("QS_NO_ROWSCALE") != nullptr;
+  if (off || m.size() != 4) return false;
+  const cd lam = std::abs(m[0]) >= std::abs(m[1]) ? m[0] : m[1];
+  if (lam == cd(0, 0)) return false;
+  const cd ilam(-lam.imag(), lam.real());
+  std::vector<cd> r(4);
+  int units = 0;
+  for (int k = 0; k < 4; k++) {
+    const cd z = m[k];
+    if (z == cd(0, 0)) r[k] = cd(0, 0);
+    else if (z == lam) r[k] = cd(1, 0), units++;
+    else if (z == -lam) r[k] = cd(-1, 0), units++;
+    else if (z == ilam) r[k] = cd(0, 1), units++;
+    else if (z == -ilam) r[k] = cd(0, -1), units++;
+    else r[k] = z / lam;
+  }
+  // row 0 holds lam itself; the gain needs a unit in row 1 too (one-row
+  // savings are offset by the complex ratios that appear)
+  auto unit = [](const cd& z) {
+    return (z.imag() == 0.0 && std::abs(z.real()) == 1.0) || (z.real() == 0.0 && std::abs(z.imag()) == 1.0);
+  };
+  if (units < 2 || !(unit(r[2]) || unit(r[3]))) return false;
+  m.swap(r);
+  *lam_out = lam;
+  return true;
+}
+
 // FP64 instructions per output amplitude of an UNCONTROLLED op: a
 // unit-scaled matrix needs only complex additions (nnz - 1 per row).
 static double mat_cost_unc(const std::vector<cd>& m) {
@@ -1442,6 +1478,8 @@ int encode_pass(const PassPlan& p, int rank, std::vector<unsigned char>& out, st
           std::vector<cd> unit;
           if (op.cmask == 0 && !op.is_h && !op.is_x && unit_scaled(pm, &lam, &unit)) {
             pm.swap(unit);
+            lam_total *= lam;
+          } else if (t == 1 && op.cmask == 0 && !op.is_h && !op.is_x && row_scale_1q(pm, &lam)) {
             lam_total *= lam;
           }
         }
