@@ -89,16 +89,25 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # the timed region of a short workload can be ~50 ms: wait until
+            # the sampler is producing before it starts
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
 
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+
+    def mark(self):
+        """Start of the timed region: only samples from here on count."""
+        self.n0 = len(self.lines)
 
     def stop(self):
         if self.proc is None:
@@ -111,7 +120,10 @@ class ClockSampler:
         self.t.join(timeout=2)
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        n0 = getattr(self, "n0", 0)
+        # samples of the timed region; a region shorter than the 20 ms
+        # sampling interval keeps the sample just before it
+        for ln in (self.lines[n0:] if len(self.lines) > n0 else self.lines[max(0, n0 - 1):]):
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -362,6 +374,7 @@ def main():
     # times over the timed steps (qs_set_timing(ctx, 2)): the loop holds
     # nothing but the steps, the totals are read once afterwards
     sim.set_timing(2)
+    clocks.mark()
     ev0.record(stream)
     for _ in range(args.steps):
         step()
