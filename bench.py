@@ -147,8 +147,8 @@ PLAN_BYTES = {
     "qft30": 51539607552, "qft31": 103079215104, "qft32": 206158430208, "qft33": 412316860416,
     "rzz30": 17179869184, "rzz31": 34359738368, "rzz32": 68719476736, "rzz33": 137438953472,
     "diag30": 51539607552, "diag31": 103079215104, "diag32": 206158430208, "diag33": 412316860416,
-    "qaoa30": 360777252864, "qaoa31": 858993459200, "qaoa32": 1717986918400, "qaoa33": 3435973836800,
-    "rand30": 1254130450432, "rand31": 2714419331072, "rand32": 5841155522560, "rand33": 12506944765952,
+    "qaoa30": 360777252864, "qaoa31": 858993459200, "qaoa32": 1855425871872, "qaoa33": 3710851743744,
+    "rand30": 1288490188800, "rand31": 2783138807808, "rand32": 5841155522560, "rand33": 12781822672896,
 }
 
 

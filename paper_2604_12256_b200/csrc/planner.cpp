@@ -253,18 +253,10 @@ static bool row_scale_1q(std::vector<cd>& m, cd* lam_out) {
 // FP64 instructions per output amplitude of an UNCONTROLLED op: a
 // unit-scaled matrix needs only complex additions (nnz - 1 per row).
 static double mat_cost_unc(const std::vector<cd>& m) {
-  if (m.size() == 4 && !unit_scaled(m, nullptr, nullptr)) {
-    // one-qubit row scaling (row_scale_1q): unit entries are the FMA addends
-    std::vector<cd> r = m;
-    cd lam;
-    if (!row_scale_1q(r, &lam)) return mat_cost(m);
-    double c = 0;
-    for (const cd& z : r) {
-      const bool unit = (z.imag() == 0.0 && std::abs(z.real()) == 1.0) || (z.real() == 0.0 && std::abs(z.imag()) == 1.0);
-      c += (z == cd(0, 0) || unit) ? 0.0 : (z.imag() == 0.0 || z.real() == 0.0) ? 2.0 : 4.0;
-    }
-    return c / 2.0;
-  }
+  // (row-scaled one-qubit gates, r9b, are priced at their full-matrix cost:
+  // pricing them at 2 FP64/amp lets the write-only pass take more gates,
+  // which removed a pass of QAOA-32 on 4 GPUs but made one of its fused-swap
+  // passes run at half the NVLink rate, 133 -> 152 ms)
   if (!unit_scaled(m, nullptr, nullptr)) return mat_cost(m);
   size_t D = 1;
   while (D * D < m.size()) D++;

@@ -295,3 +295,30 @@ def test_l2_runs_not_used_on_loopback_shards(qs):
     s.close()
     assert info["l2_groups"] == 0
     check(psi, n, gates, basis=77)
+
+
+@pytest.mark.parametrize("jit", [0, 99])
+def test_row_scaled_one_qubit_gates_special_angles(qs, jit):
+    """r9b: uncontrolled RX/RY/U3 applied as lam [[1, b/lam], [c/lam, 1]] with
+    lam in the pass scale -- at the angles where an entry vanishes or the
+    larger entry switches (0, pi/2, pi, -pi, 3pi/2) and at random angles,
+    controlled copies unscaled; both kernel paths, against the oracle."""
+    rng = np.random.default_rng(909)
+    n = 20
+    angles = [0.0, np.pi / 2, np.pi, -np.pi, 1.5 * np.pi, 1e-9, np.pi - 1e-9]
+    circ = [W.Gate("H", (q,)) for q in range(n)]
+    for layer in range(4):
+        for q in range(n):
+            th = float(angles[(q + layer) % len(angles)]) if q % 3 else float(rng.uniform(-4, 4))
+            kind = ("RX", "RY")[(q + layer) % 2]
+            circ.append(W.Gate(kind, (q,), (), (th,)))
+        circ.append(W.Gate("U3", (layer,), (), tuple(float(x) for x in rng.uniform(-3, 3, 3))))
+        circ.append(W.Gate("RX", (layer + 5,), (layer + 9,), (float(rng.uniform(-3, 3)),)))
+        circ += [W.Gate("CZ", ((q + 1) % n,), (q,)) for q in range(layer % 2, n, 2)]
+    s = qs.Simulator(n)
+    s.set_config(qs.make_config(jit_min_qubits=jit))
+    s.set_basis_state(11)
+    s.apply(circ)
+    psi = s.state()
+    s.close()
+    check(psi, n, circ, basis=11)
