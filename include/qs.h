@@ -92,7 +92,7 @@ typedef struct {
   uint32_t flags;       /* QS_OPT_* (QS_OPT_ALL)                             */
   int32_t jit_min_qubits; /* passes over >= this many local qubits run as
                              per-pass NVRTC-specialised kernels; 0 = all,
-                             > 40 = none.  Default 18 (env QS_JIT=0/1
+                             > 40 = none.  Default 13 (env QS_JIT=0/1
                              overrides the default to none / all).          */
   int32_t l2_block_qubits; /* two-level blocking ("accommodated in
                              the higher-level memory", "within the

@@ -60,11 +60,13 @@ void jit_stats(double* compile_ms, uint64_t* compiles, uint64_t* disk_hits);
 
 namespace {
 // QS_JIT: "0" interpreter kernels only, "1" specialise every chunk/dense/diag
-// pass, unset/"auto": specialise passes over >= 18 local qubits (the tiny
-// sub-state and test passes stay on the interpreter kernels).
+// pass, unset/"auto": specialise every pass over more than kSmallMax local
+// qubits, booster sub-states included (round 2: the 15-qubit sub-state
+// passes of QFT-30 on the interpreter cost ~0.1 ms per circuit, 8.93 ->
+// 8.84 ms; the others tie; round 1 kept them on the interpreter, 18).
 int jit_default_min() {
   const char* e = getenv("QS_JIT");
-  if (!e || !*e || !strcmp(e, "auto")) return 18;
+  if (!e || !*e || !strcmp(e, "auto")) return qs::kSmallMax + 1;
   return atoi(e) ? 0 : 99;
 }
 

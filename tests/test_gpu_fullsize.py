@@ -1,7 +1,7 @@
 """GPU parity at sizes where the specialised kernels run in steady state
 (-m gpu; VERDICT r1 "Next round" item 1).
 
-Every test here uses the DEFAULT configuration (passes over >= 18 local
+Every test here uses the DEFAULT configuration (passes over >= 13 local
 qubits run as NVRTC-specialised kernels) at n = 23-26, i.e. 2^11-2^14
 chunks per pass: with the 148-296 CTA grids each CTA processes 7-55 chunks,
 so the refill ring (mbarrier phases >= 1, the two-group "issued" wait), the
