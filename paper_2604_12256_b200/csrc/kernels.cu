@@ -811,6 +811,27 @@ __global__ void qs_kshape_table(const unsigned char* __restrict__ blob, u64* __r
   // thread per (row, column) entry diverged across columns and ran ~8x
   // slower (QFT-30's write-only pass table: 148 us on the critical path)
   const int apad = (v.n_ang + 1) & ~1;
+  if (P.n_chunks < 4096) {
+    // few rows (sub-state passes): one thread per (row, column) entry keeps
+    // the GPU busy (8 rows x all columns per thread took 12 vs 5 us)
+    const int ncol = v.n_ang + v.n_cis;
+    const u64 total = P.n_chunks * (u64)ncol;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (u64)gridDim.x * blockDim.x) {
+      const u64 c = i / (u64)ncol;
+      const int t = (int)(i - c * (u64)ncol);
+      const u64 cphys = deposit_runs(P, c) | rank_base;
+      u64* row = tab + c * (u64)v.width;
+      if (t < v.n_ang) {
+        row[t] = shape_level1(S, T, v.ang[t], cphys);
+      } else {
+        const int e = t - v.n_ang;
+        u64 th = 0;
+        for (int q = v.cis_beg[e]; q < v.cis_beg[e + 1]; q++) th += shape_level1(S, T, v.cis_shape[q], cphys);
+        reinterpret_cast<double2*>(row + apad)[e] = cis_turns(th);
+      }
+    }
+    return;
+  }
   for (u64 c = (u64)blockIdx.x * blockDim.x + threadIdx.x; c < P.n_chunks; c += (u64)gridDim.x * blockDim.x) {
     const u64 cphys = deposit_runs(P, c) | rank_base;
     u64* row = tab + c * (u64)v.width;
@@ -825,7 +846,7 @@ __global__ void qs_kshape_table(const unsigned char* __restrict__ blob, u64* __r
 
 cudaError_t launch_shape_table(const unsigned char* dblob, u64* tab, u64 rank_base, u64 n_chunks,
                                const TabCols& v, cudaStream_t st) {
-  u64 blocks = (n_chunks + 255) / 256;
+  u64 blocks = (n_chunks * (n_chunks < 4096 ? (u64)(v.n_ang + v.n_cis) : 1ull) + 255) / 256;
   u64 cap = (u64)num_sms() * 8;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
